@@ -1,0 +1,193 @@
+/*
+ * pi.h -- C ABI of libpi, a B200-native (sm_100a) implementation of the hot path of
+ * arXiv 2406.16091 "cutoff-limited pairwise particle interactions on a cell grid with
+ * few particles per cell".
+ *
+ * Citations: "PAPER.md:L" is line L of the paper's LaTeX source (the paper itself, not
+ * shipped here); section / algorithm / equation named alongside.
+ *
+ * What the library computes (§2): for every particle i, the interactions
+ * with all j != i such that r_ij < r_c through a kernel K(r_ij); the grid of cells of
+ * width >= r_c (§3) only restricts the candidates to the 27 neighbour cells
+ * (§5.1).  The pipeline (§2):
+ *   a1 cell index of every particle from its position             -> pi_bin
+ *   a2 per-cell counts with atomics                               -> pi_bin
+ *   a3 prefix sum of the counts (+ M_C, §5.1)       -> pi_bin
+ *   a4 out-of-place move into cell-sorted "secondary" arrays      -> pi_bin
+ *   a5 launch configuration (sub-box / pencil sizing)             -> pi_interact
+ *   a6 interactions with the same and neighbouring cells          -> pi_interact
+ *   a7 position update ("their positions are updated", :65)       -> pi_step
+ *   a8 X-slab ghost / migration exchange (north star, nranks > 1) -> pi_bin / pi_step
+ *
+ * Conventions
+ *   Pointers: every particle/cell array argument is a CUDA DEVICE pointer owned by the
+ *     caller, unless the function name ends in _host (pinned or pageable host memory).
+ *     Float arrays must be 16-byte aligned (vectorised loads); NULL is allowed only where
+ *     stated.
+ *   Ownership: libpi never allocates device memory.  All of its state lives in the
+ *     caller-provided workspace (pi_workspace_bytes); pi_create only carves it up.
+ *     pi_bin copies its inputs (out of place) and never writes them.
+ *   Asynchrony: calls enqueue on cfg.stream and return without synchronising, except
+ *     pi_create (NCCL bootstrap when nranks > 1), pi_get_stats and the *_host calls.
+ *     pi_bin / pi_interact / pi_step perform no allocation and no host synchronisation,
+ *     so they can be captured in a CUDA graph.
+ *   Errors: status codes, nothing is thrown across the ABI; pi_last_error() gives text.
+ *     Errors detected on the device (particle outside the box, NaN position, capacity
+ *     overflow) set a sticky flag reported by the next pi_get_stats (PI_EDEVICE).
+ *   Threading: one context per (process, GPU); a context is not thread safe.
+ */
+#ifndef PI_H_
+#define PI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PI_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PI_API __attribute__((visibility("default")))
+#else
+#define PI_API
+#endif
+
+typedef struct pi_ctx_s *pi_ctx;
+
+typedef enum {
+  PI_OK = 0,
+  PI_EINVAL = 1,         /* bad argument (see each call)                                  */
+  PI_ECAPACITY = 2,      /* n (or arrivals) exceed cfg.capacity                           */
+  PI_EINAPPLICABLE = 3,  /* strategy cannot run (PAPER.md:276 sub-box < 27 cells, :354)   */
+  PI_ECUDA = 4,          /* CUDA runtime error (text in pi_last_error)                     */
+  PI_ENCCL = 5,          /* NCCL error                                                     */
+  PI_ESTATE = 6,         /* call out of order (e.g. pi_interact before pi_bin)             */
+  PI_EDEVICE = 7         /* sticky device-side error flag was set (see pi_stats.flags)     */
+} pi_status;
+
+/* Interaction kernel K(r).  PAPER.md:51-52 (§2) names "the Gaussian function"; the paper's
+ * measured kernel is Lennard-Jones (Eq. 1), listed as next work.
+ *   PI_K_GAUSSIAN : K(r) = exp(-r^2 / (2 sigma^2)), sigma = kparam[0] (0 -> r_c / 3);
+ *                   phi_i = sum_j q_j K(r_ij),  F_i = (q_i / sigma^2) sum_j q_j K(r_ij) (x_i - x_j)
+ *                   (F_i = -grad_i of q_i sum_j q_j K).
+ *   PI_K_INDICATOR: phi_i = sum_{j: r_ij < r_c} q_j, F = 0        (test kernel: exact counts)
+ *   PI_K_CANDIDATE: phi_i = sum_{j in 27 cells, j != i} q_j, F = 0 (test kernel: no cutoff)    */
+typedef enum { PI_K_GAUSSIAN = 0, PI_K_INDICATOR = 1, PI_K_CANDIDATE = 2 } pi_kernel;
+
+/* Interaction strategy (a6).
+ *   PI_A_GLOBAL  : Par-Part-NoLoop (Alg. 1, §4.1): one thread per target,
+ *                  sources read from global memory through L1/L2.  The paper's baseline.
+ *   PI_A_FULLLOAD: All-in-SM / full load (Alg. 4, §5.1): a 3-D sub-box
+ *                  plus its ghost shell staged in shared memory (cp.async.bulk), local
+ *                  offsets from the global prefix array.
+ *   PI_A_XPENCIL : X-pencil (Alg. 5, §5.2), re-designed to stream the
+ *                  9 neighbour pencils of a target pencil along X through shared memory.
+ *   PI_A_AUTO    : the fastest measured strategy for the workload (currently X-pencil).   */
+typedef enum { PI_A_GLOBAL = 0, PI_A_FULLLOAD = 1, PI_A_XPENCIL = 2, PI_A_AUTO = 3 } pi_algo;
+
+typedef struct {
+  /* Global grid (PAPER.md:54-56 §2, :93 §3).  Cells are cubes of width cell_width; the box
+   * is [origin, origin + dims * cell_width); linear cell index is X-fastest,
+   * lin = cx + dims[0] * (cy + dims[1] * cz).  Boundaries are open.      */
+  float origin[3];
+  float cell_width;          /* must be >= r_c; > 0                          */
+  int32_t dims[3];           /* each >= 1; dims[0] divisible by nranks                      */
+  float r_c;                 /* cutoff radius, > 0                                           */
+  int32_t kernel;            /* pi_kernel                                                    */
+  float kparam[4];           /* kernel parameters; Gaussian: kparam[0] = sigma (0 -> r_c/3)  */
+  int64_t capacity;          /* max particles resident on this rank (owned + ghosts)        */
+  void *stream;              /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)  */
+  int32_t rank, nranks;      /* X-slab decomposition (north star); nranks >= 1               */
+  const void *nccl_unique_id;/* 128-byte ncclUniqueId shared by all ranks; NULL iff nranks==1 */
+  int32_t reserved[8];       /* must be zero                                                 */
+} pi_config;
+
+typedef struct {
+  int64_t n_owned;           /* particles owned by this rank after the last pi_bin/pi_step  */
+  int64_t n_ghost;           /* ghost (source-only) particles staged from neighbour ranks   */
+  int32_t max_per_cell;      /* M_C of the last binning                       */
+  int32_t flags;             /* sticky device error bits: 1 out-of-box/NaN position,
+                                2 capacity overflow, 4 internal                              */
+  int64_t candidates;        /* ordered candidate pairs of the last interaction (C)          */
+  int64_t fallback_cells;    /* target cells that took the global-memory fallback            */
+  int64_t migrants_in;       /* particles received by the last migration (nranks > 1)       */
+  int64_t migrants_out;
+  int64_t steps;             /* pi_step calls so far                                          */
+  int64_t reserved[8];
+} pi_stats;
+
+/* Tuning knobs of the launch configuration (a5).  Zero fields mean "library default".   */
+typedef struct {
+  int32_t xpencil_len;       /* X-pencil: target cells per block along X                    */
+  int32_t xpencil_cap;       /* X-pencil: staged particles per round (shared memory)        */
+  int32_t fullload_box[3];   /* full load: target sub-box (interior) dims                   */
+  int32_t fullload_cap;      /* full load: staged particles per block                       */
+  int32_t threads;           /* threads per block of the staged kernels                     */
+  int32_t reserved[8];
+} pi_tuning;
+
+PI_API int32_t pi_abi_version(void);
+
+/* Bytes of device workspace a context with this configuration needs (0 on bad config).   */
+PI_API size_t pi_workspace_bytes(const pi_config *cfg);
+
+/* Create a context inside `workspace` (device memory, >= pi_workspace_bytes, 256-B
+ * aligned).  With nranks > 1 this is collective over the ranks (NCCL communicator
+ * bootstrap from cfg->nccl_unique_id) and synchronises.
+ * Errors: PI_EINVAL (cell_width < r_c, dims <= 0, dims[0] % nranks, r_c <= 0, workspace
+ * too small or misaligned, NULL out), PI_ENCCL, PI_ECUDA.                                  */
+PI_API pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_ctx *out);
+PI_API pi_status pi_destroy(pi_ctx ctx);
+PI_API pi_status pi_set_stream(pi_ctx ctx, void *stream);
+PI_API pi_status pi_set_tuning(pi_ctx ctx, const pi_tuning *t);
+
+/* a1-a4 (+a8 when nranks > 1): bin n particles (SoA, device pointers, §2) into
+ * the context's cell-sorted state.  id may be NULL (ids default to 0..n-1).  Positions must
+ * lie in the box (this rank's slab when nranks > 1); a particle on the upper face clamps
+ * into the last cell.  Errors: PI_EINVAL (n < 0, NULL or misaligned pointer with n > 0),
+ * PI_ECAPACITY (n > capacity).                                                              */
+PI_API pi_status pi_bin(pi_ctx ctx, int64_t n, const float *x, const float *y, const float *z, const float *q,
+                 const int32_t *id);
+
+/* a5-a6: interactions of every binned particle with its candidates (same and 26
+ * neighbouring cells, j != i, r_ij < r_c).  Outputs are written in the caller order of the
+ * last pi_bin (length n); any output pointer may be NULL (results stay in the context's
+ * sorted state, see pi_get_particles).  Errors: PI_ESTATE (no binning yet, or the sorted
+ * state came from pi_step and caller-order outputs were requested), PI_EINAPPLICABLE.      */
+PI_API pi_status pi_interact(pi_ctx ctx, pi_algo algo, float *phi, float *fx, float *fy, float *fz);
+
+/* One time step: bin the current positions, interact, then x <- x + dt F with reflecting
+ * walls (reading of PAPER.md:65), in sorted order.  Collective when
+ * nranks > 1 (migration + ghost exchange over NCCL).  The first call after pi_bin reuses
+ * that binning.                                                                             */
+PI_API pi_status pi_step(pi_ctx ctx, pi_algo algo, float dt);
+
+/* End-to-end call on HOST buffers: copies x,y,z,q (n floats each) host->device, bins,
+ * interacts and copies phi,fx,fy,fz device->host, then synchronises the stream.  Host
+ * buffers should be pinned for full bandwidth.  Outputs in input order; NULL allowed.      */
+PI_API pi_status pi_run_host(pi_ctx ctx, pi_algo algo, int64_t n, const float *x, const float *y, const float *z,
+                      const float *q, float *phi, float *fx, float *fy, float *fz);
+
+/* Introspection (device pointers, async, any may be NULL):
+ *   cell_of[n]  cell index of each particle of the last pi_bin, caller order   (a1)
+ *   counts[Nc]  particles per cell (local grid when nranks > 1)                (a2)
+ *   offsets[Nc+1] exclusive prefix, offsets[Nc] = n                            (a3)
+ *   perm[n]     sorted slot -> caller index of the last pi_bin                  (a4)          */
+PI_API pi_status pi_get_binning(pi_ctx ctx, int32_t *cell_of, int32_t *counts, int32_t *offsets, int32_t *perm);
+
+/* Sorted state (device pointers, async, any may be NULL): positions, values, ids and the
+ * last interaction's outputs of the n_owned owned particles, in cell-sorted order.          */
+PI_API pi_status pi_get_particles(pi_ctx ctx, float *x, float *y, float *z, float *q, int32_t *id, float *phi,
+                           float *fx, float *fy, float *fz);
+
+/* Synchronises the stream and fills *out.  Returns PI_EDEVICE if a sticky flag is set.      */
+PI_API pi_status pi_get_stats(pi_ctx ctx, pi_stats *out);
+
+PI_API const char *pi_last_error(pi_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PI_H_ */

@@ -1,0 +1,405 @@
+// C ABI of libpi (include/pi.h): context, workspace carving, call sequencing.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "pi_internal.cuh"
+
+using namespace pi;
+
+namespace {
+
+constexpr size_t ALIGN = 256;
+
+size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
+
+struct Layout {
+  size_t ctl, counts, offsets, tiles, rec, sid, perm, urec, uid, rank, outs, io, total;
+};
+
+Layout make_layout(long long ncells, long long cap) {
+  Layout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + bytes);
+    return at;
+  };
+  L.ctl = take(sizeof(DevCtl));
+  L.counts = take(sizeof(int32_t) * (size_t)(ncells + 4));
+  L.offsets = take(sizeof(int32_t) * (size_t)(ncells + 4));
+  L.tiles = take(sizeof(unsigned long long) * (size_t)scan_tiles(ncells));
+  L.rec = take(sizeof(float4) * (size_t)cap);
+  L.sid = take(sizeof(int32_t) * (size_t)cap);
+  L.perm = take(sizeof(int32_t) * (size_t)cap);
+  L.urec = take(sizeof(float4) * (size_t)cap);
+  L.uid = take(sizeof(int32_t) * (size_t)cap);
+  L.rank = take(sizeof(int32_t) * (size_t)cap);
+  L.outs = take(sizeof(float4) * (size_t)cap);
+  L.io = take(sizeof(float) * 8 * (size_t)cap);
+  L.total = o;
+  return L;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---- small utility kernels (introspection / host path) ----
+__global__ void k_unpack(long long n, const float4 *__restrict__ rec, const int32_t *__restrict__ ids,
+                         const float4 *__restrict__ outs, float *x, float *y, float *z, float *q, int32_t *id,
+                         float *phi, float *fx, float *fy, float *fz) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float4 r = rec[i];
+    if (x) x[i] = r.x;
+    if (y) y[i] = r.y;
+    if (z) z[i] = r.z;
+    if (q) q[i] = r.w;
+    if (id) id[i] = ids[i];
+    if (outs) {
+      float4 o = outs[i];
+      if (phi) phi[i] = o.x;
+      if (fx) fx[i] = o.y;
+      if (fy) fy[i] = o.z;
+      if (fz) fz[i] = o.w;
+    }
+  }
+}
+
+__global__ void k_binning_export(long long n, long long ncells, const float4 *__restrict__ rec,
+                                 const int32_t *__restrict__ perm, const int32_t *__restrict__ offsets, Geom g,
+                                 int32_t *cell_of, int32_t *counts, int32_t *offs_out, int32_t *perm_out) {
+  long long stride = (long long)gridDim.x * blockDim.x;
+  long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long i = t0; i < n; i += stride) {
+    if (cell_of) {
+      bool bad = false;
+      float4 r = rec[i];
+      cell_of[perm[i]] = cell_lin(g, r.x, r.y, r.z, bad);
+    }
+    if (perm_out) perm_out[i] = perm[i];
+  }
+  for (long long c = t0; c <= ncells; c += stride) {
+    if (offs_out) offs_out[c] = offsets[c];
+    if (counts && c < ncells) counts[c] = offsets[c + 1] - offsets[c];
+  }
+}
+
+int blocks_for(long long n, int t) {
+  long long b = (n + t - 1) / t;
+  if (b > 148LL * 8) b = 148LL * 8;
+  return b < 1 ? 1 : (int)b;
+}
+
+}  // namespace
+
+struct pi_ctx_s {
+  pi_config cfg;
+  pi_tuning tune;
+  Geom g;
+  KParams kp;
+  cudaStream_t stream;
+  Layout lay;
+  unsigned char *ws;
+  DevCtl *ctl;
+  int32_t *counts, *offsets, *sid, *perm, *uid, *rank;
+  unsigned long long *tiles;
+  float4 *rec, *urec, *outs;
+  float *io;
+  long long n;       // owned particles
+  int state;         // 0 empty, 1 binned from pi_bin, 2 sorted state from pi_step (U pending)
+  bool need_bin;     // pi_step must re-bin U first
+  bool interacted;
+  long long steps;
+  char err[512];
+};
+
+static pi_status fail(pi_ctx c, pi_status s, const char *fmt, ...) {
+  if (c) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->err, sizeof(c->err), fmt, ap);
+    va_end(ap);
+  }
+  return s;
+}
+
+static pi_status cuda_check(pi_ctx c, cudaError_t e, const char *where) {
+  if (e == cudaSuccess) return PI_OK;
+  return fail(c, PI_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+static bool config_ok(const pi_config *cfg, char *why, size_t n) {
+  if (!cfg) { snprintf(why, n, "cfg is NULL"); return false; }
+  for (int a = 0; a < 3; ++a)
+    if (cfg->dims[a] <= 0) { snprintf(why, n, "dims must be >= 1"); return false; }
+  if (!(cfg->cell_width > 0.f)) { snprintf(why, n, "cell_width must be > 0"); return false; }
+  if (!(cfg->r_c > 0.f)) { snprintf(why, n, "r_c must be > 0"); return false; }
+  if (cfg->r_c > cfg->cell_width) { snprintf(why, n, "cell_width must be >= r_c (PAPER.md:93)"); return false; }
+  if (cfg->kernel < 0 || cfg->kernel > 2) { snprintf(why, n, "unknown kernel"); return false; }
+  if (cfg->capacity < 0 || cfg->capacity > (1LL << 31) - 64) { snprintf(why, n, "capacity out of range"); return false; }
+  if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) { snprintf(why, n, "bad rank/nranks"); return false; }
+  if (cfg->dims[0] % cfg->nranks) { snprintf(why, n, "dims[0] must be divisible by nranks"); return false; }
+  if (cfg->nranks > 1) { snprintf(why, n, "nranks > 1 requires the multi-GPU build (pi_mgpu)"); return false; }
+  long long nc = (long long)cfg->dims[0] * cfg->dims[1] * cfg->dims[2];
+  if (nc > (1LL << 30)) { snprintf(why, n, "too many cells"); return false; }
+  return true;
+}
+
+extern "C" {
+
+int32_t pi_abi_version(void) { return PI_ABI_VERSION; }
+
+size_t pi_workspace_bytes(const pi_config *cfg) {
+  char why[256];
+  if (!config_ok(cfg, why, sizeof(why))) return 0;
+  long long nc = (long long)cfg->dims[0] * cfg->dims[1] * cfg->dims[2];
+  return make_layout(nc, cfg->capacity > 0 ? cfg->capacity : 1).total;
+}
+
+pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_ctx *out) {
+  char why[256];
+  if (!out) return PI_EINVAL;
+  *out = nullptr;
+  if (!config_ok(cfg, why, sizeof(why))) return PI_EINVAL;
+  long long nc = (long long)cfg->dims[0] * cfg->dims[1] * cfg->dims[2];
+  Layout lay = make_layout(nc, cfg->capacity > 0 ? cfg->capacity : 1);
+  if (!workspace || ws_bytes < lay.total || (reinterpret_cast<uintptr_t>(workspace) & (ALIGN - 1))) return PI_EINVAL;
+  pi_ctx c = new (std::nothrow) pi_ctx_s();
+  if (!c) return PI_EINVAL;
+  c->cfg = *cfg;
+  memset(&c->tune, 0, sizeof(c->tune));
+  c->stream = reinterpret_cast<cudaStream_t>(cfg->stream);
+  c->lay = lay;
+  c->ws = reinterpret_cast<unsigned char *>(workspace);
+  c->ctl = reinterpret_cast<DevCtl *>(c->ws + lay.ctl);
+  c->counts = reinterpret_cast<int32_t *>(c->ws + lay.counts);
+  c->offsets = reinterpret_cast<int32_t *>(c->ws + lay.offsets);
+  c->tiles = reinterpret_cast<unsigned long long *>(c->ws + lay.tiles);
+  c->rec = reinterpret_cast<float4 *>(c->ws + lay.rec);
+  c->sid = reinterpret_cast<int32_t *>(c->ws + lay.sid);
+  c->perm = reinterpret_cast<int32_t *>(c->ws + lay.perm);
+  c->urec = reinterpret_cast<float4 *>(c->ws + lay.urec);
+  c->uid = reinterpret_cast<int32_t *>(c->ws + lay.uid);
+  c->rank = reinterpret_cast<int32_t *>(c->ws + lay.rank);
+  c->outs = reinterpret_cast<float4 *>(c->ws + lay.outs);
+  c->io = reinterpret_cast<float *>(c->ws + lay.io);
+  // geometry (one rank: local grid == global grid)
+  Geom &g = c->g;
+  g.ox = cfg->origin[0]; g.oy = cfg->origin[1]; g.oz = cfg->origin[2];
+  g.w = cfg->cell_width;
+  g.inv_w = 1.0f / cfg->cell_width;  // contract C3: fl32(1/w), IEEE division on the host
+  g.nx = cfg->dims[0]; g.ny = cfg->dims[1]; g.nz = cfg->dims[2];
+  g.ncells = nc;
+  g.lx = g.ox; g.ly = g.oy; g.lz = g.oz;
+  g.hx = g.ox + (float)g.nx * g.w;
+  g.hy = g.oy + (float)g.ny * g.w;
+  g.hz = g.oz + (float)g.nz * g.w;
+  KParams &k = c->kp;
+  k.kernel = cfg->kernel;
+  k.rc = cfg->r_c;
+  k.rc2 = cfg->r_c * cfg->r_c;
+  float sigma = cfg->kparam[0] > 0.f ? cfg->kparam[0] : cfg->r_c / 3.0f;
+  k.sigma = sigma;
+  k.inv_s2 = (float)(1.0 / ((double)sigma * (double)sigma));
+  k.c2 = (float)(1.4426950408889634 / (2.0 * (double)sigma * (double)sigma));
+  k.s = (float)std::sqrt((double)k.c2);
+  k.s_inv = (float)(1.0 / std::sqrt((double)k.c2));
+  // zero the control block, counts (the scan keeps them zero afterwards) and scan status
+  cudaError_t e = cudaMemsetAsync(c->ws, 0, lay.rec, c->stream);
+  if (e != cudaSuccess) {
+    pi_status s = cuda_check(c, e, "pi_create memset");
+    delete c;
+    return s;
+  }
+  *out = c;
+  return PI_OK;
+}
+
+pi_status pi_destroy(pi_ctx c) {
+  delete c;
+  return PI_OK;
+}
+
+pi_status pi_set_stream(pi_ctx c, void *stream) {
+  if (!c) return PI_EINVAL;
+  c->stream = reinterpret_cast<cudaStream_t>(stream);
+  return PI_OK;
+}
+
+pi_status pi_set_tuning(pi_ctx c, const pi_tuning *t) {
+  if (!c || !t) return PI_EINVAL;
+  c->tune = *t;
+  return PI_OK;
+}
+
+static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, const float *z, const float *q,
+                        const int32_t *id, const float4 *rec_in) {
+  BinArgs a{};
+  a.n = n;
+  a.x = x; a.y = y; a.z = z; a.q = q;
+  a.rec_in = rec_in;
+  a.id_in = id;
+  a.cell_of = nullptr;
+  a.rank = c->rank;
+  a.counts = c->counts;
+  a.offsets = c->offsets;
+  a.tile_status = c->tiles;
+  a.rec_out = c->rec;
+  a.sid_out = c->sid;
+  a.perm_out = rec_in ? nullptr : c->perm;
+  a.ctl = c->ctl;
+  return cuda_check(c, launch_bin(c->g, a, c->stream), "pi_bin");
+}
+
+pi_status pi_bin(pi_ctx c, int64_t n, const float *x, const float *y, const float *z, const float *q,
+                 const int32_t *id) {
+  if (!c) return PI_EINVAL;
+  if (n < 0) return fail(c, PI_EINVAL, "n < 0");
+  if (n > c->cfg.capacity) return fail(c, PI_ECAPACITY, "n = %lld exceeds capacity %lld", (long long)n,
+                                       (long long)c->cfg.capacity);
+  if (n > 0 && (!x || !y || !z || !q)) return fail(c, PI_EINVAL, "NULL position/value pointer");
+  if (n > 0 && (!aligned16(x) || !aligned16(y) || !aligned16(z) || !aligned16(q)))
+    return fail(c, PI_EINVAL, "x, y, z, q must be 16-byte aligned");
+  pi_status s = do_bin(c, n, x, y, z, q, id, nullptr);
+  if (s != PI_OK) return s;
+  c->n = n;
+  c->state = 1;
+  c->need_bin = false;
+  c->interacted = false;
+  return PI_OK;
+}
+
+static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, float *fy, float *fz, bool integrate,
+                             float dt) {
+  InteractArgs a{};
+  a.n = c->n;
+  a.rec = c->rec;
+  a.offsets = c->offsets;
+  a.ctl = c->ctl;
+  a.out.sorted = c->outs;
+  a.out.perm = (phi || fx || fy || fz) ? c->perm : nullptr;
+  a.out.phi = phi; a.out.fx = fx; a.out.fy = fy; a.out.fz = fz;
+  a.out.upd = integrate ? c->urec : nullptr;
+  a.out.sid = c->sid;
+  a.out.uid = c->uid;
+  a.out.dt = dt;
+  a.tx_len = c->tune.xpencil_len;
+  a.tx_cap = c->tune.xpencil_cap;
+  a.threads = c->tune.threads;
+  a.fb[0] = c->tune.fullload_box[0]; a.fb[1] = c->tune.fullload_box[1]; a.fb[2] = c->tune.fullload_box[2];
+  a.fb_cap = c->tune.fullload_cap;
+  cudaError_t e = cudaMemsetAsync(&c->ctl->candidates, 0, 2 * sizeof(unsigned long long), c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "pi_interact memset");
+  if (algo == PI_A_AUTO) algo = PI_A_XPENCIL;
+  switch (algo) {
+    case PI_A_GLOBAL: e = launch_interact_global(c->g, c->kp, a, c->stream); break;
+    case PI_A_XPENCIL: e = launch_interact_xpencil(c->g, c->kp, a, c->stream); break;
+    case PI_A_FULLLOAD: e = launch_interact_fullload(c->g, c->kp, a, c->stream); break;
+    default: return fail(c, PI_EINVAL, "unknown algo %d", (int)algo);
+  }
+  if (e == cudaErrorNotSupported) return fail(c, PI_EINAPPLICABLE, "strategy not applicable to this grid");
+  return cuda_check(c, e, "pi_interact");
+}
+
+pi_status pi_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, float *fy, float *fz) {
+  if (!c) return PI_EINVAL;
+  if (c->state == 0) return fail(c, PI_ESTATE, "pi_interact before pi_bin");
+  bool caller = phi || fx || fy || fz;
+  if (c->state != 1 && caller) return fail(c, PI_ESTATE, "caller-order outputs need a pi_bin binning");
+  if (c->need_bin) return fail(c, PI_ESTATE, "sorted state is stale after pi_step (call pi_step or pi_bin)");
+  pi_status s = do_interact(c, algo, phi, fx, fy, fz, false, 0.f);
+  if (s == PI_OK) c->interacted = true;
+  return s;
+}
+
+pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
+  if (!c) return PI_EINVAL;
+  if (c->state == 0) return fail(c, PI_ESTATE, "pi_step before pi_bin");
+  if (!std::isfinite(dt)) return fail(c, PI_EINVAL, "dt must be finite");
+  if (c->need_bin) {
+    pi_status s = do_bin(c, c->n, nullptr, nullptr, nullptr, nullptr, c->uid, c->urec);
+    if (s != PI_OK) return s;
+  }
+  pi_status s = do_interact(c, algo, nullptr, nullptr, nullptr, nullptr, true, dt);
+  if (s != PI_OK) return s;
+  c->state = 2;
+  c->need_bin = true;
+  c->interacted = true;
+  c->steps++;
+  return PI_OK;
+}
+
+pi_status pi_run_host(pi_ctx c, pi_algo algo, int64_t n, const float *x, const float *y, const float *z,
+                      const float *q, float *phi, float *fx, float *fy, float *fz) {
+  if (!c) return PI_EINVAL;
+  if (n < 0 || n > c->cfg.capacity) return fail(c, PI_ECAPACITY, "n out of range");
+  if (n > 0 && (!x || !y || !z || !q)) return fail(c, PI_EINVAL, "NULL host input");
+  size_t cap = (size_t)c->cfg.capacity;
+  float *dx = c->io, *dy = c->io + cap, *dz = c->io + 2 * cap, *dq = c->io + 3 * cap;
+  float *dphi = c->io + 4 * cap, *dfx = c->io + 5 * cap, *dfy = c->io + 6 * cap, *dfz = c->io + 7 * cap;
+  size_t bytes = sizeof(float) * (size_t)n;
+  cudaError_t e;
+  const float *src[4] = {x, y, z, q};
+  float *dst[4] = {dx, dy, dz, dq};
+  for (int k = 0; k < 4; ++k)
+    if (n > 0 && (e = cudaMemcpyAsync(dst[k], src[k], bytes, cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
+      return cuda_check(c, e, "pi_run_host H2D");
+  pi_status s = pi_bin(c, n, dx, dy, dz, dq, nullptr);
+  if (s != PI_OK) return s;
+  s = pi_interact(c, algo, phi ? dphi : nullptr, fx ? dfx : nullptr, fy ? dfy : nullptr, fz ? dfz : nullptr);
+  if (s != PI_OK) return s;
+  float *hout[4] = {phi, fx, fy, fz};
+  float *dout[4] = {dphi, dfx, dfy, dfz};
+  for (int k = 0; k < 4; ++k)
+    if (n > 0 && hout[k] &&
+        (e = cudaMemcpyAsync(hout[k], dout[k], bytes, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+      return cuda_check(c, e, "pi_run_host D2H");
+  return cuda_check(c, cudaStreamSynchronize(c->stream), "pi_run_host sync");
+}
+
+pi_status pi_get_binning(pi_ctx c, int32_t *cell_of, int32_t *counts, int32_t *offsets, int32_t *perm) {
+  if (!c) return PI_EINVAL;
+  if (c->state == 0) return fail(c, PI_ESTATE, "no binning yet");
+  if (c->need_bin && (cell_of || perm)) return fail(c, PI_ESTATE, "binning superseded by pi_step");
+  if (c->state != 1 && (cell_of || perm)) return fail(c, PI_ESTATE, "cell_of/perm refer to a pi_bin input");
+  long long n = c->n;
+  long long work = n > c->g.ncells + 1 ? n : c->g.ncells + 1;
+  k_binning_export<<<blocks_for(work, 256), 256, 0, c->stream>>>(n, c->g.ncells, c->rec, c->perm, c->offsets, c->g,
+                                                                 cell_of, counts, offsets, perm);
+  return cuda_check(c, cudaGetLastError(), "pi_get_binning");
+}
+
+pi_status pi_get_particles(pi_ctx c, float *x, float *y, float *z, float *q, int32_t *id, float *phi, float *fx,
+                           float *fy, float *fz) {
+  if (!c) return PI_EINVAL;
+  if (c->state == 0) return fail(c, PI_ESTATE, "no particles yet");
+  const float4 *rec = c->need_bin ? c->urec : c->rec;
+  const int32_t *ids = c->need_bin ? c->uid : c->sid;
+  if (c->n > 0)
+    k_unpack<<<blocks_for(c->n, 256), 256, 0, c->stream>>>(c->n, rec, ids, c->interacted ? c->outs : nullptr, x, y,
+                                                           z, q, id, phi, fx, fy, fz);
+  return cuda_check(c, cudaGetLastError(), "pi_get_particles");
+}
+
+pi_status pi_get_stats(pi_ctx c, pi_stats *out) {
+  if (!c || !out) return PI_EINVAL;
+  DevCtl h;
+  cudaError_t e = cudaMemcpyAsync(&h, c->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "pi_get_stats");
+  memset(out, 0, sizeof(*out));
+  out->n_owned = c->n;
+  out->n_ghost = 0;
+  out->max_per_cell = h.max_per_cell;
+  out->flags = h.flags;
+  out->candidates = (int64_t)h.candidates;
+  out->fallback_cells = (int64_t)h.fallback_cells;
+  out->steps = c->steps;
+  if (h.flags) return fail(c, PI_EDEVICE, "device error flags 0x%x", h.flags);
+  return PI_OK;
+}
+
+const char *pi_last_error(pi_ctx c) { return c ? c->err : "NULL context"; }
+
+}  // extern "C"

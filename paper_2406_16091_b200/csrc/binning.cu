@@ -1,0 +1,321 @@
+// a1-a4: binning of the particles into the cell grid (§2, Fig. 1).
+//
+//   k_count   a1 + a2: cell index from the position ("without moving the particles",
+//             :60) and per-cell counts "by using atomic operations" (:62).  The atomic's
+//             return value is kept as the particle's rank inside its cell, so the
+//             scatter needs no second atomic.  Warp-aggregated with __match_any_sync:
+//             lanes that fall in the same cell issue one atomic (pays off on the nearly
+//             sorted input of pi_step and on clustered clouds).
+//   k_scan    a3: "prefix sum ... where the particles that belong to a given cell should
+//             be located" (:63) -- one pass, decoupled look-back over tiles of 4096
+//             counts, warp-shuffle scans inside a tile; also M_C, "the maximum number of
+//             particles in a cell" retained while computing the prefix sum (:242).  It
+//             zeroes the counts it consumed so the next binning needs no memset.
+//   k_scatter a4: "move the particles in a secondary array (not in-place)" (:64): slot =
+//             offsets[cell] + rank; writes one 16-byte (x, y, z, q) record per particle
+//             (a full 16-B store instead of four 4-B scattered stores) plus its id.
+#include "pi_internal.cuh"
+
+namespace pi {
+
+namespace {
+
+constexpr int COUNT_THREADS = 256;
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;  // 4096 cells per tile
+
+// Warp-aggregated atomic increment; returns this lane's rank inside its cell.
+__device__ __forceinline__ int agg_increment(int32_t *counts, int lin, bool valid) {
+  const unsigned full = 0xffffffffu;
+  int key = valid ? lin : -1 - (int)(threadIdx.x & 31);   // invalid lanes never group
+  unsigned peers = __match_any_sync(full, key);
+  int leader = __ffs(peers) - 1;
+  int lane = threadIdx.x & 31;
+  int base = 0;
+  if (valid && lane == leader) base = atomicAdd(counts + lin, __popc(peers));
+  base = __shfl_sync(full, base, leader);
+  return base + __popc(peers & lanemask_lt());
+}
+
+// a1 + a2 over SoA input (pi_bin): 4 particles per thread through float4 loads.
+__global__ void __launch_bounds__(COUNT_THREADS) k_count_soa(long long n, const float *__restrict__ x,
+                                                              const float *__restrict__ y,
+                                                              const float *__restrict__ z, Geom g,
+                                                              int32_t *__restrict__ counts,
+                                                              int32_t *__restrict__ rank,
+                                                              int32_t *__restrict__ cell_of, DevCtl *ctl) {
+  long long nvec = (n + 3) >> 2;
+  bool bad = false;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v - (threadIdx.x & 31) < nvec;
+       v += (long long)gridDim.x * blockDim.x) {
+    long long i0 = v << 2;
+    float xs[4], ys[4], zs[4];
+    bool in = v < nvec;
+    if (in && i0 + 3 < n) {
+      float4 a = __ldg(reinterpret_cast<const float4 *>(x) + v);
+      float4 b = __ldg(reinterpret_cast<const float4 *>(y) + v);
+      float4 c = __ldg(reinterpret_cast<const float4 *>(z) + v);
+      xs[0] = a.x; xs[1] = a.y; xs[2] = a.z; xs[3] = a.w;
+      ys[0] = b.x; ys[1] = b.y; ys[2] = b.z; ys[3] = b.w;
+      zs[0] = c.x; zs[1] = c.y; zs[2] = c.z; zs[3] = c.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bool ok = in && i0 + j < n;
+        xs[j] = ok ? x[i0 + j] : 0.f;
+        ys[j] = ok ? y[i0 + j] : 0.f;
+        zs[j] = ok ? z[i0 + j] : 0.f;
+      }
+    }
+    int rk[4], lin[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      bool ok = in && i0 + j < n;
+      bool b = false;
+      lin[j] = cell_lin(g, xs[j], ys[j], zs[j], b);
+      bad |= ok && b;
+      rk[j] = agg_increment(counts, lin[j], ok);
+    }
+    if (in && i0 + 3 < n) {
+      reinterpret_cast<int4 *>(rank)[v] = make_int4(rk[0], rk[1], rk[2], rk[3]);
+      if (cell_of) reinterpret_cast<int4 *>(cell_of)[v] = make_int4(lin[0], lin[1], lin[2], lin[3]);
+    } else if (in) {
+      for (int j = 0; j < 4; ++j)
+        if (i0 + j < n) {
+          rank[i0 + j] = rk[j];
+          if (cell_of) cell_of[i0 + j] = lin[j];
+        }
+    }
+  }
+  if (bad) atomicOr(&ctl->flags, FLAG_OUT_OF_BOX);
+}
+
+// a1 + a2 over AoS records (pi_step re-binning of the updated sorted state).
+__global__ void __launch_bounds__(COUNT_THREADS) k_count_aos(long long n, const float4 *__restrict__ rec, Geom g,
+                                                              int32_t *__restrict__ counts,
+                                                              int32_t *__restrict__ rank, DevCtl *ctl) {
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    bool ok = i < n;
+    float4 r = ok ? __ldg(rec + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    bool b = false;
+    int lin = cell_lin(g, r.x, r.y, r.z, b);
+    bad |= ok && b;
+    int rk = agg_increment(counts, lin, ok);
+    if (ok) rank[i] = rk;
+  }
+  if (bad) atomicOr(&ctl->flags, FLAG_OUT_OF_BOX);
+}
+
+// ---------------------------------------------------------------------------------
+// a3: single-pass prefix scan with decoupled look-back.
+// Status word per tile: [epoch:30 | flag:2 | value:32]; flag 1 = tile aggregate,
+// 2 = inclusive prefix.  The epoch (bumped by the last block of each launch) makes
+// stale words of earlier launches invisible, so the status array is never cleared.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t *__restrict__ counts,
+                                                       int32_t *__restrict__ offsets,
+                                                       unsigned long long *__restrict__ status, int num_tiles,
+                                                       DevCtl *ctl) {
+  __shared__ int s_tile;
+  __shared__ int s_warp[SCAN_THREADS / 32];
+  __shared__ int s_prefix;
+  __shared__ unsigned s_epoch;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    s_tile = atomicAdd(&ctl->scan_tile_ctr, 1);
+    s_epoch = *((volatile unsigned *)&ctl->scan_epoch);
+  }
+  __syncthreads();
+  const int tile = s_tile;
+  const unsigned long long etag = ((unsigned long long)(s_epoch & 0x3fffffffu)) << 34;
+  const long long base = (long long)tile * SCAN_TILE + (long long)tid * SCAN_ITEMS;
+
+  int v[SCAN_ITEMS];
+  if (base + SCAN_ITEMS <= ncells) {
+    int4 *p = reinterpret_cast<int4 *>(counts + base);
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS / 4; ++k) {
+      int4 a = p[k];
+      v[4 * k] = a.x; v[4 * k + 1] = a.y; v[4 * k + 2] = a.z; v[4 * k + 3] = a.w;
+      p[k] = make_int4(0, 0, 0, 0);  // leave zeroed counts for the next binning
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+      long long c = base + k;
+      v[k] = c < ncells ? counts[c] : 0;
+      if (c < ncells) counts[c] = 0;
+    }
+  }
+  int mx = 0, sum = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) { mx = max(mx, v[k]); sum += v[k]; }
+  // warp inclusive scan of the thread sums
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 31) s_warp[warp] = incl;
+  if (lane == 0) atomicMax(&ctl->mc_slot[s_epoch & 1], mx);
+  __syncthreads();
+  if (warp == 0) {
+    int ws = lane < SCAN_THREADS / 32 ? s_warp[lane] : 0;
+    int wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < SCAN_THREADS / 32) s_warp[lane] = wi - ws;  // exclusive warp offsets
+    int tile_total = __shfl_sync(0xffffffffu, wi, SCAN_THREADS / 32 - 1);
+    // publish the aggregate, then look back
+    int prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st_relaxed(status + tile, etag | (2ull << 32) | (unsigned)tile_total);
+    } else {
+      if (lane == 0) st_relaxed(status + tile, etag | (1ull << 32) | (unsigned)tile_total);
+      int look = tile - 1;
+      while (true) {
+        int t = look - lane;
+        unsigned long long w = 0;
+        unsigned flag = 0;
+        if (t >= 0) {
+          do {
+            w = ld_relaxed(status + t);
+            flag = ((w >> 34) == (etag >> 34)) ? (unsigned)((w >> 32) & 3ull) : 0u;
+          } while (flag == 0);
+        } else {
+          flag = 2;  // below tile 0: nothing
+        }
+        unsigned incl_mask = __ballot_sync(0xffffffffu, flag == 2);
+        int first = incl_mask ? __ffs(incl_mask) - 1 : 32;   // nearest inclusive predecessor
+        int val = (t >= 0 && lane <= first) ? (int)(unsigned)(w & 0xffffffffull) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (first < 32) break;
+        look -= 32;
+      }
+      if (lane == 0) st_relaxed(status + tile, etag | (2ull << 32) | (unsigned)(prefix + tile_total));
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  int run = s_prefix + s_warp[warp] + incl - sum;
+  int outv[SCAN_ITEMS];
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) { outv[k] = run; run += v[k]; }
+  if (base + SCAN_ITEMS <= ncells) {
+    int4 *p = reinterpret_cast<int4 *>(offsets + base);  // offsets is 16-B aligned
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS / 4; ++k)
+      p[k] = make_int4(outv[4 * k], outv[4 * k + 1], outv[4 * k + 2], outv[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k)
+      if (base + k < ncells) offsets[base + k] = outv[k];
+  }
+  if (base <= ncells - 1 && ncells - 1 < base + SCAN_ITEMS) offsets[ncells] = run;  // offsets[Nc] = N
+  // last block: publish M_C, reset counters, advance the epoch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    int done = atomicAdd(&ctl->scan_done_ctr, 1);
+    if (done == num_tiles - 1) {
+      __threadfence();
+      unsigned e = s_epoch;
+      int m = atomicAdd(&ctl->mc_slot[e & 1], 0);
+      ctl->max_per_cell = m;
+      ctl->mc_slot[(e + 1) & 1] = 0;
+      ctl->scan_tile_ctr = 0;
+      ctl->scan_done_ctr = 0;
+      __threadfence();
+      atomicAdd(&ctl->scan_epoch, 1u);
+    }
+  }
+}
+
+// a4: out-of-place scatter.  SoA input (pi_bin) or AoS records (pi_step).
+template <bool AOS>
+__global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const float *__restrict__ x,
+                                                            const float *__restrict__ y,
+                                                            const float *__restrict__ z,
+                                                            const float *__restrict__ q,
+                                                            const float4 *__restrict__ rec_in,
+                                                            const int32_t *__restrict__ id_in, Geom g,
+                                                            const int32_t *__restrict__ rank,
+                                                            const int32_t *__restrict__ offsets,
+                                                            float4 *__restrict__ rec_out,
+                                                            int32_t *__restrict__ sid_out,
+                                                            int32_t *__restrict__ perm_out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 r;
+    if (AOS) {
+      r = __ldg(rec_in + i);
+    } else {
+      r = make_float4(__ldg(x + i), __ldg(y + i), __ldg(z + i), __ldg(q + i));
+    }
+    bool b = false;
+    int lin = cell_lin(g, r.x, r.y, r.z, b);
+    int slot = __ldg(offsets + lin) + __ldg(rank + i);
+    rec_out[slot] = r;
+    sid_out[slot] = id_in ? __ldg(id_in + i) : (int32_t)i;
+    if (perm_out) perm_out[slot] = (int32_t)i;
+  }
+}
+
+int grid_for(long long work, int threads) {
+  long long b = (work + threads - 1) / threads;
+  long long cap = 148LL * 16;  // persistent-ish cap: 16 blocks per SM
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+int scan_tiles(long long ncells) { return (int)((ncells + SCAN_TILE - 1) / SCAN_TILE); }
+
+cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
+  if (a.n > 0) {
+    if (a.rec_in) {
+      k_count_aos<<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.rec_in, g, a.counts, a.rank,
+                                                                         a.ctl);
+    } else {
+      k_count_soa<<<grid_for((a.n + 3) / 4, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.x, a.y, a.z, g,
+                                                                                   a.counts, a.rank, a.cell_of,
+                                                                                   a.ctl);
+    }
+  }
+  int tiles = scan_tiles(g.ncells);
+  k_scan<<<tiles, SCAN_THREADS, 0, s>>>(g.ncells, a.counts, a.offsets, a.tile_status, tiles, a.ctl);
+  if (a.n > 0) {
+    if (a.rec_in)
+      k_scatter<true><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
+          a.n, nullptr, nullptr, nullptr, nullptr, a.rec_in, a.id_in, g, a.rank, a.offsets, a.rec_out, a.sid_out,
+          a.perm_out);
+    else
+      k_scatter<false><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
+          a.n, a.x, a.y, a.z, a.q, nullptr, a.id_in, g, a.rank, a.offsets, a.rec_out, a.sid_out, a.perm_out);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace pi

@@ -1,0 +1,95 @@
+// a6.1: Par-Part-NoLoop, the paper's global-memory baseline (Alg. 1, PAPER.md:105-137,
+// §4.1): one thread per target particle, "no loop over the particles, and no use of the
+// shared memory" (:109); the sources of the 27 neighbour cells are read from global
+// memory through L1/L2 (:110); "part_source != part_target" (:127) is an identity test;
+// 128 threads per block (:556).
+//
+// B200 specifics: the cell-sorted state is one 16-B (x, y, z, q) record per particle, so a
+// source is one LDG.128; the 3 cells of a neighbour row (dx = -1..1) are contiguous in the
+// X-fastest order, so the 27 cells are walked as 9 contiguous runs.
+// r^2 is computed directly (dx^2 + dy^2 + dz^2) and the cutoff test is strict (<).
+#include "pi_internal.cuh"
+
+namespace pi {
+namespace {
+
+constexpr int PPNL_THREADS = 128;
+
+template <int KERNEL>
+__global__ void __launch_bounds__(PPNL_THREADS) k_interact_global(long long n, const float4 *__restrict__ rec,
+                                                                  const int32_t *__restrict__ offsets, Geom g,
+                                                                  KParams kp, OutDesc out, DevCtl *ctl) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long cand = 0;
+  if (t < n) {
+    const float4 me = __ldg(rec + t);
+    bool bad = false;
+    const int cx = cell_coord(me.x, g.ox, g.inv_w, g.nx, bad);
+    const int cy = cell_coord(me.y, g.oy, g.inv_w, g.ny, bad);
+    const int cz = cell_coord(me.z, g.oz, g.inv_w, g.nz, bad);
+    const int xlo = max(cx - 1, 0), xhi = min(cx + 1, g.nx - 1);
+    float phi = 0.f, fx = 0.f, fy = 0.f, fz = 0.f;
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int z = cz + dz;
+      if (z < 0 || z >= g.nz) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int y = cy + dy;
+        if (y < 0 || y >= g.ny) continue;
+        const long long row = (long long)g.nx * (y + (long long)g.ny * z);
+        const int lo = __ldg(offsets + row + xlo);
+        const int hi = __ldg(offsets + row + xhi + 1);
+        cand += (unsigned long long)(hi - lo);
+        for (int s = lo; s < hi; ++s) {
+          if (s == t) continue;
+          const float4 o = __ldg(rec + s);
+          const float dx = me.x - o.x, dy2 = me.y - o.y, dz2 = me.z - o.z;
+          const float r2 = fmaf(dz2, dz2, fmaf(dy2, dy2, dx * dx));
+          if (KERNEL == PI_K_CANDIDATE) {
+            phi += o.w;
+          } else if (r2 < kp.rc2) {
+            if (KERNEL == PI_K_INDICATOR) {
+              phi += o.w;
+            } else {
+              const float w = o.w * ex2_approx(-kp.c2 * r2);
+              phi += w;
+              fx = fmaf(w, dx, fx);
+              fy = fmaf(w, dy2, fy);
+              fz = fmaf(w, dz2, fz);
+            }
+          }
+        }
+      }
+    }
+    cand -= 1;  // self
+    if (KERNEL == PI_K_GAUSSIAN) {
+      const float s = me.w * kp.inv_s2;
+      fx *= s; fy *= s; fz *= s;
+    } else {
+      fx = fy = fz = 0.f;
+    }
+    write_output(out, g, (int)t, me, phi, fx, fy, fz);
+  }
+  // candidates (C) for the statistics
+  for (int o = 16; o > 0; o >>= 1) cand += __shfl_xor_sync(0xffffffffu, cand, o);
+  if ((threadIdx.x & 31) == 0 && cand) atomicAdd(&ctl->candidates, cand);
+}
+
+}  // namespace
+
+cudaError_t launch_interact_global(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s) {
+  if (a.n <= 0) return cudaSuccess;
+  int blocks = (int)((a.n + PPNL_THREADS - 1) / PPNL_THREADS);
+  switch (k.kernel) {
+    case PI_K_GAUSSIAN:
+      k_interact_global<PI_K_GAUSSIAN><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl);
+      break;
+    case PI_K_INDICATOR:
+      k_interact_global<PI_K_INDICATOR><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl);
+      break;
+    default:
+      k_interact_global<PI_K_CANDIDATE><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace pi

@@ -1,0 +1,160 @@
+// Internal declarations of libpi (sm_100a).  Not part of the ABI (see include/pi.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pi.h"
+
+namespace pi {
+
+// ------------------------------------------------------------------------------------
+// Geometry and kernel constants, passed by value to every kernel.
+// ------------------------------------------------------------------------------------
+struct Geom {
+  float ox, oy, oz;   // origin of the LOCAL grid (== global unless nranks > 1)
+  float w, inv_w;     // cell width and fl32(1/w) (contract C3)
+  int nx, ny, nz;     // local grid dims
+  long long ncells;
+  float hx, hy, hz;   // upper faces of the box this rank owns (integration walls)
+  float lx, ly, lz;   // lower faces
+};
+
+struct KParams {
+  int kernel;         // pi_kernel
+  float rc, rc2;
+  float sigma, inv_s2;  // 1/sigma^2
+  float c2;             // log2(e) / (2 sigma^2): K = 2^(-c2 r^2)
+  float s, s_inv;       // sqrt(c2) and 1/sqrt(c2): coordinate scale of the staged kernels
+};
+
+// Device-resident control / statistics block (in the workspace).
+struct DevCtl {
+  int scan_tile_ctr;     // dynamic tile ids of the look-back scan
+  int scan_done_ctr;     // blocks finished (last one resets)
+  unsigned scan_epoch;   // tags the look-back status words of one launch
+  int mc_slot[2];        // atomicMax slots for M_C, indexed by epoch parity
+  int max_per_cell;      // M_C of the last scan
+  int flags;             // sticky error bits
+  int pad0;
+  unsigned long long candidates;
+  unsigned long long fallback_cells;
+  unsigned long long pad[4];
+};
+
+enum : int { FLAG_OUT_OF_BOX = 1, FLAG_CAPACITY = 2, FLAG_INTERNAL = 4 };
+
+// ------------------------------------------------------------------------------------
+// a1: cell index, contract C3: c = clamp(floor(fl32(fl32(x - o) * inv_w)), 0, N - 1).
+// __fsub_rn / __fmul_rn forbid FMA contraction, so the result is bit-identical to the
+// per-operation-rounded definition.  NaN maps to cell 0 and raises FLAG_OUT_OF_BOX.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int cell_coord(float x, float o, float inv_w, int nd, bool &bad) {
+  float t = __fmul_rn(__fsub_rn(x, o), inv_w);
+  float f = floorf(t);
+  bad |= !(f == f);
+  int c = (f >= 0.f) ? ((f < (float)nd) ? (int)f : nd - 1) : 0;
+  return c;
+}
+
+__device__ __forceinline__ int cell_lin(const Geom &g, float x, float y, float z, bool &bad) {
+  int cx = cell_coord(x, g.ox, g.inv_w, g.nx, bad);
+  int cy = cell_coord(y, g.oy, g.inv_w, g.ny, bad);
+  int cz = cell_coord(z, g.oz, g.inv_w, g.nz, bad);
+  return cx + g.nx * (cy + g.ny * cz);
+}
+
+__device__ __forceinline__ float ex2_approx(float a) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Integration (a7, reading C11): x' = x + dt F, reflect at the walls, clamp into [lo, hi).
+__device__ __forceinline__ float integrate1(float x, float f, float dt, float lo, float hi) {
+  float y = fmaf(dt, f, x);
+  if (y < lo) y = lo + (lo - y);
+  if (y >= hi) y = hi - (y - hi);
+  const float below = __int_as_float(__float_as_int(hi) - 1);  // largest float < hi (hi > 0)
+  y = fminf(fmaxf(y, lo), below);
+  return y;
+}
+
+// ------------------------------------------------------------------------------------
+// Output descriptor of the interaction kernels.
+// ------------------------------------------------------------------------------------
+struct OutDesc {
+  float4 *sorted;          // [n] (phi, fx, fy, fz) in sorted order (always written)
+  const int32_t *perm;     // sorted slot -> caller index (NULL: no caller-order outputs)
+  float *phi, *fx, *fy, *fz;  // caller order (each nullable)
+  // pi_step: write integrated positions in sorted order
+  float4 *upd;             // NULL: no integration
+  const int32_t *sid;
+  int32_t *uid;
+  float dt;
+};
+
+__device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, int t, float4 rec, float phi,
+                                             float fx, float fy, float fz) {
+  o.sorted[t] = make_float4(phi, fx, fy, fz);
+  if (o.perm) {
+    int c = o.perm[t];
+    if (o.phi) o.phi[c] = phi;
+    if (o.fx) o.fx[c] = fx;
+    if (o.fy) o.fy[c] = fy;
+    if (o.fz) o.fz[c] = fz;
+  }
+  if (o.upd) {
+    float4 u;
+    u.x = integrate1(rec.x, fx, o.dt, g.lx, g.hx);
+    u.y = integrate1(rec.y, fy, o.dt, g.ly, g.hy);
+    u.z = integrate1(rec.z, fz, o.dt, g.lz, g.hz);
+    u.w = rec.w;
+    o.upd[t] = u;
+    o.uid[t] = o.sid[t];
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Launchers (host side, in the .cu files).
+// ------------------------------------------------------------------------------------
+struct BinArgs {
+  long long n;
+  const float *x, *y, *z, *q;   // SoA input (pi_bin), or NULL when rec_in is used
+  const float4 *rec_in;         // AoS input (pi_step re-binning)
+  const int32_t *id_in;         // ids (NULL -> index)
+  int32_t *cell_of;             // optional: a1 output in input order
+  int32_t *rank;                // scratch [n]
+  int32_t *counts;              // [ncells], zero on entry, zeroed again by the scan
+  int32_t *offsets;             // [ncells + 1]
+  unsigned long long *tile_status;
+  int num_tiles_cap;
+  float4 *rec_out;              // sorted records (x, y, z, q)
+  int32_t *sid_out;             // sorted ids
+  int32_t *perm_out;            // sorted slot -> input index (nullable)
+  DevCtl *ctl;
+};
+
+cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s);
+int scan_tiles(long long ncells);
+
+struct InteractArgs {
+  long long n;                  // particles in the sorted state
+  const float4 *rec;            // sorted records
+  const int32_t *offsets;       // [ncells + 1]
+  OutDesc out;
+  DevCtl *ctl;
+  int tx_len, tx_cap, threads;  // tuning (x-pencil)
+  int fb[3], fb_cap;            // tuning (full load)
+};
+
+cudaError_t launch_interact_global(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
+cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
+cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
+
+}  // namespace pi

@@ -1,0 +1,151 @@
+"""a5-a6 parity through the C ABI: every strategy and kernel against the fp64 oracle.
+
+Tolerance (north star / C10): |gpu - oracle| <= 1e-4 * sum_j |c_ij| + A_i per particle and
+component, exact 0 where nothing contributes; INDICATOR / CANDIDATE counts (q = 1) exact."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import reference as ref
+from tests._util import assert_parity, ctx_for, gpu_interact, oracle_interact, to_dev
+
+pytestmark = pytest.mark.gpu
+ALGOS = ["global", "xpencil"]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate"])
+def test_c0_full(algo, kernel):
+    """configs[0]: 4096 uniform particles, 16^3 cells, every particle vs the oracle."""
+    c = synth.make_config("c0")
+    got, ctx = gpu_interact(c, algo, kernel)
+    want = oracle_interact(c, kernel)
+    assert_parity(got, want, label=f"c0 {algo} {kernel}")
+    if kernel != "gaussian":
+        assert np.all(got[:, 1:] == 0)
+    st = ctx.stats()
+    assert st["candidates"] == int(want["C"].sum())
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_counts_exact_q1(algo):
+    c = synth.make_config("c0", qkind="ones")
+    got, _ = gpu_interact(c, algo, "indicator")
+    want = oracle_interact(c, "indicator")
+    assert np.array_equal(got[:, 0], want["P"].astype(np.float64))
+    got, _ = gpu_interact(c, algo, "candidate")
+    want = oracle_interact(c, "candidate")
+    assert np.array_equal(got[:, 0], want["C"].astype(np.float64))
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("variant", ["A", "B"])
+def test_hand2x3_exact(algo, variant):
+    """C12: dyadic coordinates; variant B has pairs at exactly r = r_c that must be excluded."""
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hand2x3.json")))
+    c = synth.hand_2x3(variant)
+    c.q = np.ones(9, np.float32)
+    got, _ = gpu_interact(c, algo, "indicator")
+    assert got[:, 0].tolist() == g["indicator_q1"]
+    got, _ = gpu_interact(c, algo, "candidate")
+    assert got[:, 0].tolist() == g["candidate_q1"]
+    c = synth.hand_2x3(variant)
+    got, _ = gpu_interact(c, algo, "indicator")
+    assert got[:, 0].tolist() == g["indicator_qj"]
+    want = oracle_interact(c, "gaussian", band=0.0)
+    got, _ = gpu_interact(c, algo, "gaussian")
+    assert_parity(got, want, label="hand gaussian")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("d", [4, 8])
+def test_lattice_exact_boundary(algo, d):
+    """C14: dyadic lattice with pairs at exactly r = r_c (band 0): interior phi/q closed form."""
+    c = synth.lattice(d)
+    got, _ = gpu_interact(c, algo, "indicator")
+    want = oracle_interact(c, "indicator", band=0.0)
+    assert np.array_equal(got[:, 0], want["P"].astype(np.float64))
+    got, _ = gpu_interact(c, algo, "gaussian")
+    want = oracle_interact(c, "gaussian", band=0.0)
+    assert_parity(got, want, label=f"lattice{d} {algo}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_degenerate(algo):
+    grid = synth.Grid(dims=(4, 4, 4), w=0.25)
+    # one particle: exactly zero
+    c = synth.Cloud(grid, np.array([0.3], np.float32), np.array([0.6], np.float32), np.array([0.9], np.float32),
+                    np.array([1.5], np.float32))
+    got, _ = gpu_interact(c, algo)
+    assert np.all(got == 0)
+    # two particles in neighbouring cells, closed form
+    c = synth.Cloud(grid, np.array([0.30, 0.40], np.float32), np.array([0.30, 0.35], np.float32),
+                    np.array([0.30, 0.28], np.float32), np.array([1.25, 0.75], np.float32))
+    got, _ = gpu_interact(c, algo)
+    assert_parity(got, oracle_interact(c), label="two")
+    # coincident distinct particles do interact (identity exclusion, K(0) = 1, F = 0)
+    c = synth.Cloud(grid, np.array([0.3, 0.3], np.float32), np.array([0.3, 0.3], np.float32),
+                    np.array([0.3, 0.3], np.float32), np.array([2.0, 3.0], np.float32))
+    got, _ = gpu_interact(c, algo)
+    assert got[0, 0] == pytest.approx(3.0, rel=1e-6) and got[1, 0] == pytest.approx(2.0, rel=1e-6)
+    assert np.all(got[:, 1:] == 0)
+    # empty
+    c = synth.Cloud(grid, *(np.zeros(0, np.float32) for _ in range(4)))
+    ctx = ctx_for(c, capacity=16)
+    ctx.bin(*to_dev(c))
+    ctx.interact(algo)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("ppc", [1, 4, 8, 20, 64])
+def test_density_sweep(algo, ppc):
+    """BASELINE configs[2] shape (particles-per-cell sweep) at oracle-friendly sizes."""
+    c = synth.scaled_uniform(ppc, (12, 10, 9), seed=240616093 + ppc)
+    got, _ = gpu_interact(c, algo)
+    assert_parity(got, oracle_interact(c), label=f"ppc{ppc} {algo}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_signed_charges(algo):
+    c = synth.make_config("c0", qkind="signed")
+    got, _ = gpu_interact(c, algo)
+    assert_parity(got, oracle_interact(c), label="signed")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_clustered_small(algo):
+    """configs[3] shape at 2^17 particles on 32^3: dense blobs exercise the staging overflow path."""
+    c = synth.clustered(1 << 17, synth.Grid(dims=(32, 32, 32), w=1 / 32), seed=240616094)
+    got, ctx = gpu_interact(c, algo)
+    sample = np.random.default_rng(1).choice(c.n, 20000, replace=False)
+    want = oracle_interact(c, targets=sample)
+    assert_parity(got[sample], want, label=f"clustered {algo}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_xpencil_tuning_shapes(algo):
+    """Staged kernel with tiny capacity (forces several rounds and the fallback) and odd lengths."""
+    c = synth.scaled_uniform(8, (20, 6, 5), seed=3)
+    want = oracle_interact(c)
+    for tune in (dict(xpencil_len=1), dict(xpencil_len=7, xpencil_cap=300), dict(xpencil_len=64),
+                 dict(xpencil_len=16, xpencil_cap=64), dict(threads=256, xpencil_len=5)):
+        got, _ = gpu_interact(c, algo, tuning=tune)
+        assert_parity(got, want, label=f"{algo} {tune}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_c1_sampled(algo):
+    """configs[1] (2^21, 64^3, 8/cell) in the bench's launch configuration, sampled targets."""
+    c = synth.make_config("c1")
+    got, ctx = gpu_interact(c, algo)
+    sample = np.random.default_rng(2).choice(c.n, 30000, replace=False)
+    want = oracle_interact(c, targets=sample)
+    assert_parity(got[sample], want, label=f"c1 {algo}")
+    st = ctx.stats()
+    assert st["fallback_cells"] == 0 or algo == "global"
+    # property at full size: sum of forces ~ 0 (antisymmetry), relative to sum |F|
+    F = got[:, 1:]
+    assert np.all(np.abs(F.sum(0)) <= 1e-4 * np.abs(F).sum(0))
