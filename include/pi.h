@@ -125,7 +125,8 @@ typedef struct {
   int32_t fullload_box[3];   /* full load: target sub-box (interior) dims                   */
   int32_t fullload_cap;      /* full load: staged particles per block                       */
   int32_t threads;           /* threads per block of the staged kernels                     */
-  int32_t reserved[8];
+  int32_t lanes_per_pair;    /* staged kernels: lanes sharing one target pair (1, 2, 4)     */
+  int32_t reserved[7];
 } pi_tuning;
 
 PI_API int32_t pi_abi_version(void);

@@ -1,5 +1,6 @@
 // C ABI of libpi (include/pi.h): context, workspace carving, call sequencing.
 #include <cmath>
+#include <cstddef>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -287,9 +288,11 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.tx_len = c->tune.xpencil_len;
   a.tx_cap = c->tune.xpencil_cap;
   a.threads = c->tune.threads;
+  a.groups = c->tune.lanes_per_pair;
   a.fb[0] = c->tune.fullload_box[0]; a.fb[1] = c->tune.fullload_box[1]; a.fb[2] = c->tune.fullload_box[2];
   a.fb_cap = c->tune.fullload_cap;
-  cudaError_t e = cudaMemsetAsync(&c->ctl->candidates, 0, 2 * sizeof(unsigned long long), c->stream);
+  cudaError_t e = cudaMemsetAsync(&c->ctl->fallback_cells, 0,
+                                  sizeof(DevCtl) - offsetof(DevCtl, fallback_cells), c->stream);
   if (e != cudaSuccess) return cuda_check(c, e, "pi_interact memset");
   if (algo == PI_A_AUTO) algo = PI_A_XPENCIL;
   switch (algo) {
@@ -393,7 +396,9 @@ pi_status pi_get_stats(pi_ctx c, pi_stats *out) {
   out->n_ghost = 0;
   out->max_per_cell = h.max_per_cell;
   out->flags = h.flags;
-  out->candidates = (int64_t)h.candidates;
+  unsigned long long cand = 0;
+  for (int k = 0; k < CAND_SLOTS; ++k) cand += h.cand_slots[k];
+  out->candidates = (int64_t)cand;
   out->fallback_cells = (int64_t)h.fallback_cells;
   out->steps = c->steps;
   if (h.flags) return fail(c, PI_EDEVICE, "device error flags 0x%x", h.flags);

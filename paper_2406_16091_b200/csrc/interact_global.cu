@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(PPNL_THREADS) k_interact_global(long long n, c
   }
   // candidates (C) for the statistics
   for (int o = 16; o > 0; o >>= 1) cand += __shfl_xor_sync(0xffffffffu, cand, o);
-  if ((threadIdx.x & 31) == 0 && cand) atomicAdd(&ctl->candidates, cand);
+  if ((threadIdx.x & 31) == 0 && cand) atomicAdd(&ctl->cand_slots[(blockIdx.x * 4 + (threadIdx.x >> 5)) & (CAND_SLOTS - 1)], cand);
 }
 
 }  // namespace

@@ -36,10 +36,11 @@ struct DevCtl {
   int max_per_cell;      // M_C of the last scan
   int flags;             // sticky error bits
   int pad0;
-  unsigned long long candidates;
   unsigned long long fallback_cells;
-  unsigned long long pad[4];
+  unsigned long long pad[3];
+  unsigned long long cand_slots[64];  // candidates (C) of the last interaction, spread counters
 };
+constexpr int CAND_SLOTS = 64;
 
 enum : int { FLAG_OUT_OF_BOX = 1, FLAG_CAPACITY = 2, FLAG_INTERNAL = 4 };
 
@@ -149,7 +150,7 @@ struct InteractArgs {
   const int32_t *offsets;       // [ncells + 1]
   OutDesc out;
   DevCtl *ctl;
-  int tx_len, tx_cap, threads;  // tuning (x-pencil)
+  int tx_len, tx_cap, threads, groups;  // tuning (x-pencil)
   int fb[3], fb_cap;            // tuning (full load)
 };
 

@@ -1,0 +1,17 @@
+"""Run bin + interact on one config a few times (for ncu capture)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, synth
+from paper_2406_16091_b200 import Context
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
+algo = sys.argv[2] if len(sys.argv) > 2 else "xpencil"
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+c = synth.make_config(cfg)
+g = c.grid
+ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=c.n)
+t = [torch.from_numpy(v).cuda() for v in (c.x, c.y, c.z, c.q)]
+for _ in range(reps):
+    ctx.bin(*t)
+    ctx.interact(algo, out=False)
+torch.cuda.synchronize()
+print("done")
