@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the hot path of arXiv 2406.16091 on B200 (driver contract).
+
+A "step" is one pass of the whole hot path over the synthetic cloud of BASELINE.json
+configs[1] (2^21 uniform particles, 64^3 cells, 8 per cell, Gaussian K, r_c = w):
+pi_step = a1-a4 binning (cell index + counts, look-back scan + M_C, scatter), a5-a6
+interaction (X-pencil strategy by default) and a7 position update.  Inputs are resident in
+HBM; L2 is flushed (256 MiB write) between timed steps and the flush is outside the timed
+events.  The metric is candidate pair interactions per second (ordered pairs (i, j), j != i,
+in the 27 neighbour cells -- the unit of the paper's Table 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--algo xpencil|global|fullload]
+  python bench.py --impl reference ...   # the fp64 CPU oracle on a bounded sample (rank 0)
+
+N > 1 (launched with torchrun): until the X-slab exchange is enabled in the benchmark every
+rank runs an independent replica of the workload ("scaling": "weak"), timed on the device
+and reduced with MAX over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP32_PEAK_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.45: FMA lanes x SMs x max SM clock
+WORKLOAD = ("BASELINE configs[1]: 2^21 uniform particles in the unit box, 64^3 cells (8/cell), "
+            "r_c = w = 1/64, Gaussian K sigma = r_c/3, fp32")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--algo", default="xpencil")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons while the timed region runs."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self._t = None
+        self.max_mhz = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nv = pynvml
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._nv = None
+        return self
+
+    def _run(self):
+        nv = self._nv
+        names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------ helpers
+def traffic_from_profiles(algo):
+    """dram read+write bytes per launch of the interaction kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(algo)
+    except Exception:
+        return None
+
+
+def oracle_rate(cloud, seconds, threads, rng_seed=7):
+    """The fp64 cell-list oracle as it stands, on a bounded random sample of targets."""
+    import numpy as np
+    from oracle import celllist
+    celllist.set_threads(threads)
+    rng = np.random.default_rng(rng_seed)
+    probe = rng.choice(cloud.n, min(cloud.n, 20000), replace=False)
+    t0 = time.perf_counter()
+    r = celllist.interact(cloud.x, cloud.y, cloud.z, cloud.q, cloud.grid, targets=probe)
+    dt = time.perf_counter() - t0
+    per_target = dt / len(probe)
+    m = int(min(cloud.n, max(len(probe), seconds / max(per_target, 1e-9))))
+    sample = rng.choice(cloud.n, m, replace=False)
+    t0 = time.perf_counter()
+    r = celllist.interact(cloud.x, cloud.y, cloud.z, cloud.q, cloud.grid, targets=sample)
+    dt = time.perf_counter() - t0
+    cands = int(r["C"].sum())
+    return cands / dt, dict(targets=m, candidates=cands, seconds=dt)
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------------ reference arm
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import synth
+    cloud = synth.make_config(a.config)
+    cores = host_cores()
+    per_step = max(1.0, min(10.0, 120.0 / max(1, a.steps + a.warmup)))
+    rates = []
+    info = None
+    for s in range(a.warmup + a.steps):
+        rate, info = oracle_rate(cloud, per_step, cores, rng_seed=100 + s)
+        if s >= a.warmup:
+            rates.append(rate)
+    value = statistics.mean(rates)
+    unit = "candidate pair interactions/s"
+    ms = info["seconds"] * 1e3
+    line = {
+        "impl": "reference", "metric": "candidate pair interactions/s (27-cell ordered pairs)", "value": value,
+        "unit": unit, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": cloud.n, "cells": cloud.grid.ncells},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle",
+                         "sample": f"{info['targets']} random targets of the {cloud.n}-particle cloud per step "
+                                   f"(fp64 C cell list, OpenMP, {cores} threads; includes its own binning)"},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------ our arm
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2406_16091_b200 import Context
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    cloud = synth.make_config(a.config, seed_offset=1000 * rank)
+    g = cloud.grid
+    n = cloud.n
+    stream = torch.cuda.current_stream(dev)
+    ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=n, device=dev, stream=stream)
+    x, y, z, q = (torch.from_numpy(v).to(dev) for v in (cloud.x, cloud.y, cloud.z, cloud.q))
+
+    # cutoff pairs P (INDICATOR kernel, q = 1) for the algorithmic FLOP count 8 C + 10 P
+    ci = Context(g.dims, g.w, g.r_c, g.origin, kernel="indicator", capacity=n, device=dev, stream=stream)
+    ci.bin(x, y, z, torch.ones_like(q))
+    phi, *_ = ci.interact("global")
+    P = float(phi.double().sum().item())
+    del ci, phi
+
+    # dt: max |dt F| <= 0.01 w
+    ctx.bin(x, y, z, q)
+    _, fx, fy, fz = ctx.interact(a.algo)
+    fmax = float(torch.stack([fx.abs().max(), fy.abs().max(), fz.abs().max()]).max().item())
+    dt = 0.01 * g.w / max(fmax, 1e-30)
+    del fx, fy, fz
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(a.steps)]
+    ctx.bin(x, y, z, q)
+    clk = ClockSampler(dev.index or 0).__enter__()   # samples from warm-up to the end of e2e
+    for _ in range(a.warmup):
+        ctx.step(a.algo, dt)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    inter_ms, bin_ms, cands = [], [], []
+    if True:
+        for k in range(a.steps):
+            flush.zero_()                      # evict L2 (outside the timed events)
+            ev[k][0].record(stream)
+            ctx.step(a.algo, dt)
+            ev[k][1].record(stream)
+            st = ctx.stats()                   # synchronises; per-phase device times of this step
+            inter_ms.append(st["interact_ms"])
+            bin_ms.append(st["bin_ms"])
+            cands.append(st["candidates"])
+        torch.cuda.synchronize()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    if world > 1:
+        dist.barrier()
+    tot_ms = sum(step_ms)
+    tot_c = float(sum(cands))
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        c = torch.tensor([tot_c], device=dev, dtype=torch.float64)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        tot_c = float(c.item())
+    value = tot_c / (tot_ms * 1e-3)
+    C = statistics.mean(cands)
+    flop = 8.0 * C + 10.0 * P
+    int_ms = statistics.mean(inter_ms)
+    achieved = flop / (int_ms * 1e-3) / 1e12
+    bin_bytes = 48.0 * n + 12.0 * g.ncells
+
+    # end to end through the C ABI on pinned host buffers (H2D + bin + interact + D2H)
+    hx, hy, hz, hq = (torch.from_numpy(v).pin_memory() for v in (cloud.x, cloud.y, cloud.z, cloud.q))
+    ho = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(4)]
+    for _ in range(2):
+        ctx.run_host(a.algo, hx, hy, hz, hq, *ho)
+    e2e_ms = []
+    for _ in range(max(3, a.steps // 2)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.run_host(a.algo, hx, hy, hz, hq, *ho)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    c_e2e = ctx.stats()["candidates"]
+    clk.__exit__()
+    e2e_mean = statistics.mean(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_mean], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_mean = float(t.item())
+    e2e_value = c_e2e * world / (e2e_mean * 1e-3)
+
+    line = {
+        "metric": "candidate pair interactions/s (27-cell ordered pairs) and step ms",
+        "value": value,
+        "unit": "candidate pair interactions/s",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": tot_ms / a.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_per_gpu": n, "cells": g.ncells, "algo": a.algo,
+                   "step": "pi_step: bin (count+scan+scatter) + interact + integrate",
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic_from_profiles(a.algo),
+                     "kernel": f"k_interact_{a.algo}", "flop_per_launch": flop,
+                     "flop_model": "8 per candidate + 10 per cutoff pair (SURVEY.md §8(d))",
+                     "candidates": C, "cutoff_pairs": P, "kernel_ms": int_ms,
+                     "peak_basis": "2 x 128 FP32 lanes x 148 SMs x 1.965 GHz (no FP32 entry in MEASURED_PEAKS)"},
+        "phases": {"bin_ms": statistics.mean(bin_ms), "interact_ms": int_ms,
+                   "bin_gbs_algorithmic": bin_bytes / (statistics.mean(bin_ms) * 1e-3) / 1e9,
+                   "bin_bytes_model": "48 B/particle + 12 B/cell"},
+        "e2e": {"value": e2e_value, "unit": "candidate pair interactions/s", "ms": e2e_mean,
+                "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
+                "path": "pi_run_host: pinned H2D x,y,z,q -> bin -> interact -> D2H phi,F"},
+        "gpu_launches": 4 * a.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cores = host_cores()
+        rate, info = oracle_rate(cloud, a.cpu_seconds, cores)
+        line["cpu_baseline"] = {"value": rate, "unit": "candidate pair interactions/s", "cores": cores,
+                                "kind": "oracle",
+                                "sample": f"{info['targets']} random targets of the {n}-particle cloud "
+                                          f"({info['candidates']} candidates, {info['seconds']:.1f} s, fp64 C "
+                                          "cell list incl. its own binning)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

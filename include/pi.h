@@ -115,7 +115,10 @@ typedef struct {
   int64_t migrants_in;       /* particles received by the last migration (nranks > 1)       */
   int64_t migrants_out;
   int64_t steps;             /* pi_step calls so far                                          */
-  int64_t reserved[8];
+  double phase_ms[4];        /* device time of the last bin (a1-a4), interaction (a5-a7),
+                                exchange (a8) and host-path copies, from CUDA events recorded
+                                on the context stream around each phase                      */
+  int64_t reserved[4];
 } pi_stats;
 
 /* Tuning knobs of the launch configuration (a5).  Zero fields mean "library default".   */

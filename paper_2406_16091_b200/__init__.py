@@ -175,4 +175,6 @@ class Context:
         st = self._lib.pi_get_stats(self._h, ctypes.byref(s))
         if check:
             self._check(st)
-        return {k: getattr(s, k) for k, _ in L.pi_stats._fields_ if k != "reserved"}
+        d = {k: getattr(s, k) for k, _ in L.pi_stats._fields_ if k not in ("reserved", "phase_ms")}
+        d["bin_ms"], d["interact_ms"], d["exchange_ms"], d["host_copy_ms"] = (float(v) for v in s.phase_ms)
+        return d

@@ -27,7 +27,7 @@ class pi_stats(ctypes.Structure):
     _fields_ = [("n_owned", ctypes.c_int64), ("n_ghost", ctypes.c_int64), ("max_per_cell", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("candidates", ctypes.c_int64), ("fallback_cells", ctypes.c_int64),
                 ("migrants_in", ctypes.c_int64), ("migrants_out", ctypes.c_int64), ("steps", ctypes.c_int64),
-                ("reserved", ctypes.c_int64 * 8)]
+                ("phase_ms", ctypes.c_double * 4), ("reserved", ctypes.c_int64 * 4)]
 
 
 class pi_tuning(ctypes.Structure):

@@ -112,8 +112,16 @@ struct pi_ctx_s {
   bool need_bin;     // pi_step must re-bin U first
   bool interacted;
   long long steps;
+  cudaEvent_t ev[4][2];  // phase timing: 0 bin, 1 interact, 2 exchange, 3 host copies
+  bool ev_used[4];
   char err[512];
 };
+
+static void phase_begin(pi_ctx c, int k) {
+  cudaEventRecord(c->ev[k][0], c->stream);
+  c->ev_used[k] = true;
+}
+static void phase_end(pi_ctx c, int k) { cudaEventRecord(c->ev[k][1], c->stream); }
 
 static pi_status fail(pi_ctx c, pi_status s, const char *fmt, ...) {
   if (c) {
@@ -213,11 +221,24 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
     delete c;
     return s;
   }
+  for (int k = 0; k < 4; ++k)
+    for (int b = 0; b < 2; ++b) {
+      e = cudaEventCreate(&c->ev[k][b]);
+      if (e != cudaSuccess) {
+        pi_status s = cuda_check(c, e, "pi_create events");
+        pi_destroy(c);
+        return s;
+      }
+    }
   *out = c;
   return PI_OK;
 }
 
 pi_status pi_destroy(pi_ctx c) {
+  if (c)
+    for (int k = 0; k < 4; ++k)
+      for (int b = 0; b < 2; ++b)
+        if (c->ev[k][b]) cudaEventDestroy(c->ev[k][b]);
   delete c;
   return PI_OK;
 }
@@ -250,7 +271,10 @@ static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, c
   a.sid_out = c->sid;
   a.perm_out = rec_in ? nullptr : c->perm;
   a.ctl = c->ctl;
-  return cuda_check(c, launch_bin(c->g, a, c->stream), "pi_bin");
+  phase_begin(c, 0);
+  cudaError_t e = launch_bin(c->g, a, c->stream);
+  phase_end(c, 0);
+  return cuda_check(c, e, "pi_bin");
 }
 
 pi_status pi_bin(pi_ctx c, int64_t n, const float *x, const float *y, const float *z, const float *q,
@@ -295,12 +319,14 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
                                   sizeof(DevCtl) - offsetof(DevCtl, fallback_cells), c->stream);
   if (e != cudaSuccess) return cuda_check(c, e, "pi_interact memset");
   if (algo == PI_A_AUTO) algo = PI_A_XPENCIL;
+  phase_begin(c, 1);
   switch (algo) {
     case PI_A_GLOBAL: e = launch_interact_global(c->g, c->kp, a, c->stream); break;
     case PI_A_XPENCIL: e = launch_interact_xpencil(c->g, c->kp, a, c->stream); break;
     case PI_A_FULLLOAD: e = launch_interact_fullload(c->g, c->kp, a, c->stream); break;
     default: return fail(c, PI_EINVAL, "unknown algo %d", (int)algo);
   }
+  phase_end(c, 1);
   if (e == cudaErrorNotSupported) return fail(c, PI_EINAPPLICABLE, "strategy not applicable to this grid");
   return cuda_check(c, e, "pi_interact");
 }
@@ -345,6 +371,7 @@ pi_status pi_run_host(pi_ctx c, pi_algo algo, int64_t n, const float *x, const f
   cudaError_t e;
   const float *src[4] = {x, y, z, q};
   float *dst[4] = {dx, dy, dz, dq};
+  phase_begin(c, 3);
   for (int k = 0; k < 4; ++k)
     if (n > 0 && (e = cudaMemcpyAsync(dst[k], src[k], bytes, cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
       return cuda_check(c, e, "pi_run_host H2D");
@@ -358,6 +385,7 @@ pi_status pi_run_host(pi_ctx c, pi_algo algo, int64_t n, const float *x, const f
     if (n > 0 && hout[k] &&
         (e = cudaMemcpyAsync(hout[k], dout[k], bytes, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
       return cuda_check(c, e, "pi_run_host D2H");
+  phase_end(c, 3);
   return cuda_check(c, cudaStreamSynchronize(c->stream), "pi_run_host sync");
 }
 
@@ -401,6 +429,10 @@ pi_status pi_get_stats(pi_ctx c, pi_stats *out) {
   out->candidates = (int64_t)cand;
   out->fallback_cells = (int64_t)h.fallback_cells;
   out->steps = c->steps;
+  for (int k = 0; k < 4; ++k) {
+    float ms = 0.f;
+    if (c->ev_used[k] && cudaEventElapsedTime(&ms, c->ev[k][0], c->ev[k][1]) == cudaSuccess) out->phase_ms[k] = ms;
+  }
   if (h.flags) return fail(c, PI_EDEVICE, "device error flags 0x%x", h.flags);
   return PI_OK;
 }
