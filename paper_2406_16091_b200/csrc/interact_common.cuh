@@ -61,6 +61,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// 16-B asynchronous global -> shared copy (LDGSTS), bypassing L1.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Staged sources are stored as PAIRS (sources 2p and 2p+1) in two 16-B halves:
@@ -142,7 +149,7 @@ __device__ __forceinline__ void stage_pair(float4 *S, int p) {
 
 // One thread, one target (pair index pt, half ht) against source pairs [p0, p1) of S.
 // Returns (phi, sum w d) summed over both halves, self pair removed; F = -(q_t/sigma^2) sum w d.
-template <int KERNEL>
+template <int KERNEL, int UNR = 4>
 __device__ __forceinline__ float4 lane_target(const float4 *__restrict__ S, int pt, int ht, int p0, int p1,
                                               const float thr, const float mc2) {
   float xt, yt, zt;
@@ -154,12 +161,29 @@ __device__ __forceinline__ float4 lane_target(const float4 *__restrict__ S, int 
   }
   p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
   int p = p0;
-  for (; p + 2 <= p1; p += 2) {
-    const SrcPair s0 = load_pair(S, p), s1 = load_pair(S, p + 1);
-    src_eval<KERNEL>(s0, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
-    src_eval<KERNEL>(s1, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+  // 4 source pairs per iteration into two independent accumulator sets (ILP), or 2 pairs
+  // into one set when registers are the occupancy limit
+  p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
+  if (UNR == 2) {
+    for (; p + 2 <= p1; p += 2) {
+      const SrcPair s0 = load_pair(S, p), s1 = load_pair(S, p + 1);
+      src_eval<KERNEL>(s0, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+      src_eval<KERNEL>(s1, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+    }
   }
-  if (p < p1) src_eval<KERNEL>(load_pair(S, p), xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+  for (; UNR == 4 && p + 4 <= p1; p += 4) {
+    const SrcPair s0 = load_pair(S, p), s1 = load_pair(S, p + 1), s2 = load_pair(S, p + 2),
+                  s3 = load_pair(S, p + 3);
+    src_eval<KERNEL>(s0, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+    src_eval<KERNEL>(s1, xt, yt, zt, thr, mc2, phb, fxb, fyb, fzb);
+    src_eval<KERNEL>(s2, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+    src_eval<KERNEL>(s3, xt, yt, zt, thr, mc2, phb, fxb, fyb, fzb);
+  }
+  for (; p < p1; ++p) src_eval<KERNEL>(load_pair(S, p), xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+  phi = add2(phi, phb);
+  fx = add2(fx, fxb);
+  fy = add2(fy, fyb);
+  fz = add2(fz, fzb);
   // identity exclusion (Alg. 1 :127)
   const float self = self_phi<KERNEL>(load_pair(S, pt), ht, xt, yt, zt, thr, mc2);
   if (ht) phi = pk(lo(phi), hi(phi) - self);
@@ -167,57 +191,53 @@ __device__ __forceinline__ float4 lane_target(const float4 *__restrict__ S, int 
   return make_float4(lo(phi) + hi(phi), lo(fx) + hi(fx), lo(fy) + hi(fy), lo(fz) + hi(fz));
 }
 
-// Fallback for a target cell whose candidate window does not fit the staging buffer:
-// Par-Part-NoLoop over global memory, one thread per target, the whole block.
+// Fallback for a target whose cell window does not fit the staging buffer: Par-Part-NoLoop
+// over global memory (Alg. 1) for target slot t in cell (cx, cy, cz).
 template <int KERNEL>
-__device__ void block_fallback_cell(int cx, int cy, int cz, const float4 *__restrict__ rec,
-                                    const int32_t *__restrict__ offsets, const Geom &g, const KParams &kp,
-                                    const OutDesc &out, unsigned long long &cand) {
-  const long long home_row = (long long)g.nx * (cy + (long long)g.ny * cz);
-  const int t_lo = __ldg(offsets + home_row + cx), t_hi = __ldg(offsets + home_row + cx + 1);
+__device__ void fallback_target(int t, int cx, int cy, int cz, const float4 *__restrict__ rec,
+                                const int32_t *__restrict__ offsets, const Geom &g, const KParams &kp,
+                                const OutDesc &out, unsigned long long &cand) {
   const int xlo = max(cx - 1, 0), xhi = min(cx + 1, g.nx - 1);
-  for (int t = t_lo + threadIdx.x; t < t_hi; t += blockDim.x) {
-    const float4 me = __ldg(rec + t);
-    float phi = 0.f, fx = 0.f, fy = 0.f, fz = 0.f;
-    for (int dz = -1; dz <= 1; ++dz) {
-      const int z = cz + dz;
-      if (z < 0 || z >= g.nz) continue;
-      for (int dy = -1; dy <= 1; ++dy) {
-        const int y = cy + dy;
-        if (y < 0 || y >= g.ny) continue;
-        const long long row = (long long)g.nx * (y + (long long)g.ny * z);
-        const int lo_ = __ldg(offsets + row + xlo), hi_ = __ldg(offsets + row + xhi + 1);
-        cand += (unsigned long long)(hi_ - lo_);
-        for (int s = lo_; s < hi_; ++s) {
-          if (s == t) continue;
-          const float4 o = __ldg(rec + s);
-          const float dx = me.x - o.x, dy2 = me.y - o.y, dz2 = me.z - o.z;
-          const float r2 = fmaf(dz2, dz2, fmaf(dy2, dy2, dx * dx));
-          if (KERNEL == PI_K_CANDIDATE) {
+  const float4 me = __ldg(rec + t);
+  float phi = 0.f, fx = 0.f, fy = 0.f, fz = 0.f;
+  for (int dz = -1; dz <= 1; ++dz) {
+    const int z = cz + dz;
+    if (z < 0 || z >= g.nz) continue;
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int y = cy + dy;
+      if (y < 0 || y >= g.ny) continue;
+      const long long row = (long long)g.nx * (y + (long long)g.ny * z);
+      const int lo_ = __ldg(offsets + row + xlo), hi_ = __ldg(offsets + row + xhi + 1);
+      cand += (unsigned long long)(hi_ - lo_);
+      for (int s = lo_; s < hi_; ++s) {
+        if (s == t) continue;
+        const float4 o = __ldg(rec + s);
+        const float dx = me.x - o.x, dy2 = me.y - o.y, dz2 = me.z - o.z;
+        const float r2 = fmaf(dz2, dz2, fmaf(dy2, dy2, dx * dx));
+        if (KERNEL == PI_K_CANDIDATE) {
+          phi += o.w;
+        } else if (r2 < kp.rc2) {
+          if (KERNEL == PI_K_INDICATOR) {
             phi += o.w;
-          } else if (r2 < kp.rc2) {
-            if (KERNEL == PI_K_INDICATOR) {
-              phi += o.w;
-            } else {
-              const float w = o.w * ex2_approx(-kp.c2 * r2);
-              phi += w;
-              fx = fmaf(w, dx, fx);
-              fy = fmaf(w, dy2, fy);
-              fz = fmaf(w, dz2, fz);
-            }
+          } else {
+            const float w = o.w * ex2_approx(-kp.c2 * r2);
+            phi += w;
+            fx = fmaf(w, dx, fx);
+            fy = fmaf(w, dy2, fy);
+            fz = fmaf(w, dz2, fz);
           }
         }
       }
     }
-    cand -= 1;
-    if (KERNEL == PI_K_GAUSSIAN) {
-      const float s = me.w * kp.inv_s2;
-      fx *= s; fy *= s; fz *= s;
-    } else {
-      fx = fy = fz = 0.f;
-    }
-    write_output(out, g, t, me, phi, fx, fy, fz);
   }
+  cand -= 1;
+  if (KERNEL == PI_K_GAUSSIAN) {
+    const float sc = me.w * kp.inv_s2;
+    fx *= sc; fy *= sc; fz *= sc;
+  } else {
+    fx = fy = fz = 0.f;
+  }
+  write_output(out, g, t, me, phi, fx, fy, fz);
 }
 
 }  // namespace pi

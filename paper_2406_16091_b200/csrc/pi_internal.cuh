@@ -37,7 +37,8 @@ struct DevCtl {
   int flags;             // sticky error bits
   int pad0;
   unsigned long long fallback_cells;
-  unsigned long long pad[3];
+  unsigned long long xp_items;        // X-pencil work-item counter (reset before each launch)
+  unsigned long long pad[2];
   unsigned long long cand_slots[64];  // candidates (C) of the last interaction, spread counters
 };
 constexpr int CAND_SLOTS = 64;
