@@ -19,7 +19,7 @@ def state(ctx):
     return {k: v.cpu().numpy() for k, v in p.items()}
 
 
-@pytest.mark.parametrize("algo", ["global", "xpencil"])
+@pytest.mark.parametrize("algo", ["global", "xpencil", "fullload"])
 def test_step_matches_oracle(algo):
     c = synth.make_config("c0")
     g = c.grid
