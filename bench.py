@@ -12,9 +12,10 @@ in the 27 neighbour cells -- the unit of the paper's Table 1).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--algo xpencil|global|fullload]
   python bench.py --impl reference ...   # the fp64 CPU oracle on a bounded sample (rank 0)
 
-N > 1 (launched with torchrun): until the X-slab exchange is enabled in the benchmark every
-rank runs an independent replica of the workload ("scaling": "weak"), timed on the device
-and reduced with MAX over ranks.
+N > 1 (launched with torchrun): the X-slab decomposition (a8) -- rank r owns
+64 X layers of a (64 N) x 64 x 64 grid with 8 particles per cell, so per-GPU work equals the
+N = 1 workload ("scaling": "weak"); each pi_step migrates particles and exchanges ghost
+layers with the X neighbours over NCCL.  Timed on the device, MAX over ranks.
 """
 from __future__ import annotations
 
@@ -181,7 +182,7 @@ def run_ours(a):
     import torch.distributed as dist
 
     import synth
-    from paper_2406_16091_b200 import Context
+    from paper_2406_16091_b200 import Context, nccl_unique_id
 
     rank, world, local = dist_env()
     if world > 1:
@@ -189,25 +190,42 @@ def run_ours(a):
         dist.init_process_group("nccl", init_method="env://")
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
-    cloud = synth.make_config(a.config, seed_offset=1000 * rank)
+    if world > 1:
+        # X-slab decomposition (a8): rank r owns 64 X layers of a (64 N) x 64 x 64 grid, 8 per cell
+        cloud = synth.slab_uniform(8.0, (64, 64, 64), rank, world, seed=synth.SEED_BASE + 1)
+    else:
+        cloud = synth.make_config(a.config)
     g = cloud.grid
     n = cloud.n
+    cap = int(n * 1.25) + 4096 if world > 1 else n  # owned + ghosts + migration slack
     stream = torch.cuda.current_stream(dev)
-    ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=n, device=dev, stream=stream)
+
+    def make_ctx(kernel="gaussian"):
+        kw = {}
+        if world > 1:
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            kw = dict(rank=rank, nranks=world, nccl_unique_id=obj[0])
+        return Context(g.dims, g.w, g.r_c, g.origin, kernel=kernel, capacity=cap, device=dev, stream=stream, **kw)
+
+    ctx = make_ctx()
     x, y, z, q = (torch.from_numpy(v).to(dev) for v in (cloud.x, cloud.y, cloud.z, cloud.q))
 
     # cutoff pairs P (INDICATOR kernel, q = 1) for the algorithmic FLOP count 8 C + 10 P
-    ci = Context(g.dims, g.w, g.r_c, g.origin, kernel="indicator", capacity=n, device=dev, stream=stream)
+    ci = make_ctx("indicator")
     ci.bin(x, y, z, torch.ones_like(q))
     phi, *_ = ci.interact("global")
     P = float(phi.double().sum().item())
+    ci.close()
     del ci, phi
 
-    # dt: max |dt F| <= 0.01 w
+    # dt: max |dt F| <= 0.01 w, the same on every rank
     ctx.bin(x, y, z, q)
     _, fx, fy, fz = ctx.interact(a.algo)
-    fmax = float(torch.stack([fx.abs().max(), fy.abs().max(), fz.abs().max()]).max().item())
-    dt = 0.01 * g.w / max(fmax, 1e-30)
+    fm = torch.stack([fx.abs().max(), fy.abs().max(), fz.abs().max()]).max().double().reshape(1)
+    if world > 1:
+        dist.all_reduce(fm, op=dist.ReduceOp.MAX)
+    dt = 0.01 * g.w / max(float(fm.item()), 1e-30)
     del fx, fy, fz
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -221,38 +239,40 @@ def run_ours(a):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    inter_ms, bin_ms, cands = [], [], []
-    if True:
-        for k in range(a.steps):
-            flush.zero_()                      # evict L2 (outside the timed events)
-            ev[k][0].record(stream)
-            ctx.step(a.algo, dt)
-            ev[k][1].record(stream)
-            st = ctx.stats()                   # synchronises; per-phase device times of this step
-            inter_ms.append(st["interact_ms"])
-            bin_ms.append(st["bin_ms"])
-            cands.append(st["candidates"])
-        torch.cuda.synchronize()
+    inter_ms, bin_ms, exch_ms, cands, migr = [], [], [], [], []
+    for k in range(a.steps):
+        flush.zero_()                      # evict L2 (outside the timed events)
+        ev[k][0].record(stream)
+        ctx.step(a.algo, dt)
+        ev[k][1].record(stream)
+        st = ctx.stats()                   # synchronises; per-phase device times of this step
+        inter_ms.append(st["interact_ms"])
+        bin_ms.append(st["bin_ms"])
+        exch_ms.append(st["exchange_ms"])
+        cands.append(st["candidates"])
+        migr.append(st["migrants_in"])
+    torch.cuda.synchronize()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     if world > 1:
         dist.barrier()
     tot_ms = sum(step_ms)
     tot_c = float(sum(cands))
+    n_all = float(n)
     if world > 1:
         t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-        c = torch.tensor([tot_c], device=dev, dtype=torch.float64)
+        c = torch.tensor([tot_c, n_all], device=dev, dtype=torch.float64)
         dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        tot_c = float(c.item())
+        tot_c, n_all = float(c[0].item()), float(c[1].item())
     value = tot_c / (tot_ms * 1e-3)
     C = statistics.mean(cands)
     flop = 8.0 * C + 10.0 * P
     int_ms = statistics.mean(inter_ms)
     achieved = flop / (int_ms * 1e-3) / 1e12
-    bin_bytes = 48.0 * n + 12.0 * g.ncells
+    bin_bytes = 48.0 * n + 12.0 * g.ncells / world
 
-    # end to end through the C ABI on pinned host buffers (H2D + bin + interact + D2H)
+    # end to end through the C ABI on pinned host buffers (H2D + bin (+ a8) + interact + D2H)
     hx, hy, hz, hq = (torch.from_numpy(v).pin_memory() for v in (cloud.x, cloud.y, cloud.z, cloud.q))
     ho = [torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(4)]
     for _ in range(2):
@@ -267,15 +287,26 @@ def run_ours(a):
         e1.record(stream)
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
-    c_e2e = ctx.stats()["candidates"]
+    c_e2e = float(ctx.stats()["candidates"])
     clk.__exit__()
     e2e_mean = statistics.mean(e2e_ms)
     if world > 1:
         t = torch.tensor([e2e_mean], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_mean = float(t.item())
-    e2e_value = c_e2e * world / (e2e_mean * 1e-3)
+        c = torch.tensor([c_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        c_e2e = float(c.item())
+    e2e_value = c_e2e / (e2e_mean * 1e-3)
 
+    if world > 1:
+        workload = (f"X-slab weak scaling: {g.dims[0]}x{g.dims[1]}x{g.dims[2]} cells (64^3 per GPU), 8 uniform "
+                    f"particles per cell (~2^21 per GPU, {int(n_all)} total), r_c = w = 1/64, Gaussian K "
+                    "sigma = r_c/3, fp32; NCCL ghost + migration exchange every step")
+        launches = 10  # reset, migrate, append, reset, ghosts, append, count, scan, scatter, interact
+    else:
+        workload = WORKLOAD
+        launches = 4   # count, scan, scatter, interact (+ integrate fused)
     line = {
         "metric": "candidate pair interactions/s (27-cell ordered pairs) and step ms",
         "value": value,
@@ -289,10 +320,12 @@ def run_ours(a):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_per_gpu": n, "cells": g.ncells, "algo": a.algo,
-                   "step": "pi_step: bin (count+scan+scatter) + interact + integrate",
+        "config": {"workload": workload, "n_per_gpu": n, "n_total": int(n_all), "cells": g.ncells,
+                   "algo": a.algo,
+                   "step": "pi_step: bin (count+scan+scatter) + interact + integrate"
+                           + (" + a8 migration/ghost exchange (NCCL)" if world > 1 else ""),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "parallelism": "replicas" if world > 1 else "single GPU"},
+                   "parallelism": f"xslab{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic_from_profiles(a.algo),
                      "kernel": f"k_interact_{a.algo}", "flop_per_launch": flop,
@@ -300,12 +333,14 @@ def run_ours(a):
                      "candidates": C, "cutoff_pairs": P, "kernel_ms": int_ms,
                      "peak_basis": "2 x 128 FP32 lanes x 148 SMs x 1.965 GHz (no FP32 entry in MEASURED_PEAKS)"},
         "phases": {"bin_ms": statistics.mean(bin_ms), "interact_ms": int_ms,
+                   "exchange_ms": statistics.mean(exch_ms) if world > 1 else 0.0,
+                   "migrants_per_step": statistics.mean(migr) if world > 1 else 0.0,
                    "bin_gbs_algorithmic": bin_bytes / (statistics.mean(bin_ms) * 1e-3) / 1e9,
                    "bin_bytes_model": "48 B/particle + 12 B/cell"},
         "e2e": {"value": e2e_value, "unit": "candidate pair interactions/s", "ms": e2e_mean,
                 "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
                 "path": "pi_run_host: pinned H2D x,y,z,q -> bin -> interact -> D2H phi,F"},
-        "gpu_launches": 4 * a.steps,
+        "gpu_launches": launches * a.steps,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -318,6 +353,7 @@ def run_ours(a):
                                           "cell list incl. its own binning)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    ctx.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -100,7 +100,10 @@ typedef struct {
   int64_t capacity;          /* max particles resident on this rank (owned + ghosts)        */
   void *stream;              /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)  */
   int32_t rank, nranks;      /* X-slab decomposition (north star); nranks >= 1               */
-  const void *nccl_unique_id;/* 128-byte ncclUniqueId shared by all ranks; NULL iff nranks==1 */
+  const void *nccl_unique_id;/* 128-byte ncclUniqueId shared by all ranks (pi_nccl_unique_id
+                                on one rank, broadcast by the caller); NULL iff nranks == 1.
+                                Testing: "PILOCAL:<key>" links the nranks contexts of ONE
+                                process (one host thread per context) without NCCL.          */
   int32_t reserved[8];       /* must be zero                                                 */
 } pi_config;
 
@@ -109,11 +112,13 @@ typedef struct {
   int64_t n_ghost;           /* ghost (source-only) particles staged from neighbour ranks   */
   int32_t max_per_cell;      /* M_C of the last binning                       */
   int32_t flags;             /* sticky device error bits: 1 out-of-box/NaN position,
-                                2 capacity overflow, 4 internal                              */
+                                2 capacity overflow (particles or a8 messages), 4 internal
+                                (e.g. a particle moved more than one slab in one step),
+                                8 a pi_bin particle outside this rank's slab                 */
   int64_t candidates;        /* ordered candidate pairs of the last interaction (C)          */
   int64_t fallback_cells;    /* target cells that took the global-memory fallback            */
   int64_t migrants_in;       /* particles received by the last migration (nranks > 1)       */
-  int64_t migrants_out;
+  int64_t migrants_out;      /* particles sent by the last migration (nranks > 1)           */
   int64_t steps;             /* pi_step calls so far                                          */
   double phase_ms[4];        /* device time of the last bin (a1-a4), interaction (a5-a7),
                                 exchange (a8) and host-path copies, from CUDA events recorded
@@ -134,6 +139,19 @@ typedef struct {
 
 PI_API int32_t pi_abi_version(void);
 
+/* a8 X-slab decomposition (north star; the paper is single-GPU).  Rank r of P = nranks owns
+ * the global X cells [r Lx, (r+1) Lx), Lx = dims[0] / P, all Y and Z.  Its local grid has
+ * Lx + 2 X layers: local 0 and Lx + 1 are ghost layers (source-only copies of the
+ * neighbours' boundary layers), local 1..Lx are owned; local X = global X - gx_off.
+ * out[0] Lx, out[1] first owned global X cell, out[2] one past the last, out[3] local X
+ * layers, out[4] gx_off, out[5] own_lo, out[6] own_hi (local, half-open), out[7] record
+ * capacity of each a8 message.  Host only, no context needed.  Errors: PI_EINVAL.       */
+PI_API pi_status pi_slab_info(const pi_config *cfg, int64_t out[8]);
+
+/* 128-byte ncclUniqueId from the NCCL library libpi uses (libnccl.so.2, dlopen'ed).
+ * Errors: PI_EINVAL (NULL), PI_ENCCL (library missing).                                    */
+PI_API pi_status pi_nccl_unique_id(void *out128);
+
 /* Bytes of device workspace a context with this configuration needs (0 on bad config).   */
 PI_API size_t pi_workspace_bytes(const pi_config *cfg);
 
@@ -149,9 +167,11 @@ PI_API pi_status pi_set_tuning(pi_ctx ctx, const pi_tuning *t);
 
 /* a1-a4 (+a8 when nranks > 1): bin n particles (SoA, device pointers, §2) into
  * the context's cell-sorted state.  id may be NULL (ids default to 0..n-1).  Positions must
- * lie in the box (this rank's slab when nranks > 1); a particle on the upper face clamps
- * into the last cell.  Errors: PI_EINVAL (n < 0, NULL or misaligned pointer with n > 0),
- * PI_ECAPACITY (n > capacity).                                                              */
+ * lie in the box; a particle on the upper face clamps into the last cell.  nranks > 1: the
+ * call is collective, each rank passes the particles of ITS slab (pi_slab_info; others
+ * raise flag 8) and the first / last owned X layers are exchanged as ghosts before the
+ * owned + ghost particles are binned together.  Errors: PI_EINVAL (n < 0, NULL or
+ * misaligned pointer with n > 0), PI_ECAPACITY (n > capacity), PI_ENCCL.                   */
 PI_API pi_status pi_bin(pi_ctx ctx, int64_t n, const float *x, const float *y, const float *z, const float *q,
                  const int32_t *id);
 
@@ -164,8 +184,9 @@ PI_API pi_status pi_interact(pi_ctx ctx, pi_algo algo, float *phi, float *fx, fl
 
 /* One time step: bin the current positions, interact, then x <- x + dt F with reflecting
  * walls (reading of PAPER.md:65), in sorted order.  Collective when
- * nranks > 1 (migration + ghost exchange over NCCL).  The first call after pi_bin reuses
- * that binning.                                                                             */
+ * nranks > 1: before re-binning, owned particles whose updated global X cell left the slab
+ * migrate to rank -1 / +1 (at most one slab per step, else flag 4), then the ghost layers
+ * are exchanged again.  The first call after pi_bin reuses that binning.                   */
 PI_API pi_status pi_step(pi_ctx ctx, pi_algo algo, float dt);
 
 /* End-to-end call on HOST buffers: copies x,y,z,q (n floats each) host->device, bins,
@@ -178,11 +199,17 @@ PI_API pi_status pi_run_host(pi_ctx ctx, pi_algo algo, int64_t n, const float *x
  *   cell_of[n]  cell index of each particle of the last pi_bin, caller order   (a1)
  *   counts[Nc]  particles per cell (local grid when nranks > 1)                (a2)
  *   offsets[Nc+1] exclusive prefix, offsets[Nc] = n                            (a3)
- *   perm[n]     sorted slot -> caller index of the last pi_bin                  (a4)          */
+ *   perm[n]     sorted slot -> caller index of the last pi_bin                  (a4)
+ * nranks > 1: cells are LOCAL (Nc = (Lx + 2) dims[1] dims[2], see pi_slab_info), the sorted
+ * state holds n_owned + n_ghost slots, perm is -1 on ghost slots and offsets[Nc] =
+ * n_owned + n_ghost.                                                                          */
 PI_API pi_status pi_get_binning(pi_ctx ctx, int32_t *cell_of, int32_t *counts, int32_t *offsets, int32_t *perm);
 
 /* Sorted state (device pointers, async, any may be NULL): positions, values, ids and the
- * last interaction's outputs of the n_owned owned particles, in cell-sorted order.          */
+ * last interaction's outputs of the n_owned owned particles, in cell-sorted order (after
+ * pi_step: the updated positions, not yet re-binned).  nranks > 1: the owned particles
+ * only (ghosts skipped, migrants of the next step still included), order unspecified;
+ * arrays must hold pi_stats.n_owned entries.                                                */
 PI_API pi_status pi_get_particles(pi_ctx ctx, float *x, float *y, float *z, float *q, int32_t *id, float *phi,
                            float *fx, float *fy, float *fz);
 

@@ -11,7 +11,7 @@ import torch
 
 from . import _lib as L
 
-__all__ = ["Context", "PiError", "ALGOS", "KERNELS", "lib"]
+__all__ = ["Context", "PiError", "ALGOS", "KERNELS", "lib", "slab_info", "nccl_unique_id"]
 
 ALGOS = L.ALGOS
 KERNELS = L.KERNELS
@@ -26,6 +26,46 @@ class PiError(RuntimeError):
         self.status = status
         name = L.STATUS_NAMES[status] if 0 <= status < len(L.STATUS_NAMES) else str(status)
         super().__init__(f"{name}: {msg}")
+
+
+def _config(dims, cell_width, r_c=None, origin=(0.0, 0.0, 0.0), kernel="gaussian", sigma=0.0, capacity=0,
+            rank=0, nranks=1):
+    cfg = L.pi_config()
+    for a in range(3):
+        cfg.origin[a] = float(origin[a])
+        cfg.dims[a] = int(dims[a])
+    cfg.cell_width = float(cell_width)
+    cfg.r_c = float(cell_width if r_c is None else r_c)
+    cfg.kernel = L.KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+    cfg.kparam[0] = float(sigma)
+    cfg.capacity = int(capacity)
+    cfg.rank = int(rank)
+    cfg.nranks = int(nranks)
+    return cfg
+
+
+SLAB_KEYS = ("Lx", "gx_lo", "gx_hi", "nx_local", "gx_off", "own_lo", "own_hi", "msg_cap")
+
+
+def slab_info(dims, cell_width, rank, nranks, capacity=0, r_c=None, **kw):
+    """pi_slab_info: the X-slab of `rank` (a8).  Host only."""
+    cfg = _config(dims, cell_width, r_c=r_c, capacity=capacity, rank=rank, nranks=nranks, **kw)
+    if nranks > 1:
+        cfg.nccl_unique_id = ctypes.c_void_p(1)  # only checked for presence
+    out = (ctypes.c_int64 * 8)()
+    st = L.load().pi_slab_info(ctypes.byref(cfg), out)
+    if st != L.PI_OK:
+        raise PiError(st, "pi_slab_info: invalid configuration")
+    return dict(zip(SLAB_KEYS, (int(v) for v in out)))
+
+
+def nccl_unique_id() -> bytes:
+    """pi_nccl_unique_id: 128 bytes to broadcast to every rank before creating contexts."""
+    buf = ctypes.create_string_buffer(128)
+    st = L.load().pi_nccl_unique_id(buf)
+    if st != L.PI_OK:
+        raise PiError(st, "pi_nccl_unique_id failed")
+    return buf.raw
 
 
 def _ptr(t):
@@ -50,21 +90,12 @@ class Context:
         self.cell_width = float(cell_width)
         self.r_c = float(cell_width if r_c is None else r_c)
         self.origin = tuple(float(o) for o in origin)
-        cfg = L.pi_config()
-        for a in range(3):
-            cfg.origin[a] = self.origin[a]
-            cfg.dims[a] = self.dims[a]
-        cfg.cell_width = self.cell_width
-        cfg.r_c = self.r_c
-        cfg.kernel = L.KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
-        cfg.kparam[0] = float(sigma)
-        cfg.capacity = int(capacity)
+        cfg = _config(self.dims, self.cell_width, self.r_c, self.origin, kernel, sigma, capacity, rank, nranks)
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         self.stream = stream
         cfg.stream = ctypes.c_void_p(stream.cuda_stream)
-        cfg.rank = int(rank)
-        cfg.nranks = int(nranks)
+        self.rank, self.nranks = int(rank), int(nranks)
         self._uid = None
         if nccl_unique_id is not None:
             self._uid = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
@@ -81,6 +112,9 @@ class Context:
         self._h = h
         self.capacity = int(capacity)
         self.n = 0
+        self.slab = slab_info(self.dims, self.cell_width, self.rank, self.nranks, capacity, self.r_c)
+        # local grid (X-slab with ghost layers when nranks > 1)
+        self.local_dims = (self.slab["nx_local"], self.dims[1], self.dims[2])
 
     # ------------------------------------------------------------------ helpers
     def _check(self, st):
@@ -144,27 +178,38 @@ class Context:
                                           _ptr(fy), _ptr(fz)))
         self.n = n
 
+    def _slots(self):
+        """Sorted slots (owned + ghosts)."""
+        if self.nranks == 1:
+            return self.n
+        s = self.stats(check=False)
+        return s["n_owned"] + s["n_ghost"]
+
     def get_binning(self):
-        nc = self.dims[0] * self.dims[1] * self.dims[2]
+        """cell_of (caller order of the last bin), counts, offsets (local grid), perm (sorted slot -> caller
+        index, -1 on ghost slots)."""
+        nc = self.local_dims[0] * self.local_dims[1] * self.local_dims[2]
         dev = self.device
         cell_of = torch.empty(self.n, dtype=torch.int32, device=dev)
         counts = torch.empty(nc, dtype=torch.int32, device=dev)
         offsets = torch.empty(nc + 1, dtype=torch.int32, device=dev)
-        perm = torch.empty(self.n, dtype=torch.int32, device=dev)
+        perm = torch.empty(self._slots(), dtype=torch.int32, device=dev)
         self._check(self._lib.pi_get_binning(self._h, _ptr(cell_of), _ptr(counts), _ptr(offsets), _ptr(perm)))
         return cell_of, counts, offsets, perm
 
     def get_offsets(self):
-        nc = self.dims[0] * self.dims[1] * self.dims[2]
+        nc = self.local_dims[0] * self.local_dims[1] * self.local_dims[2]
         offsets = torch.empty(nc + 1, dtype=torch.int32, device=self.device)
         counts = torch.empty(nc, dtype=torch.int32, device=self.device)
         self._check(self._lib.pi_get_binning(self._h, None, _ptr(counts), _ptr(offsets), None))
         return counts, offsets
 
     def get_particles(self):
+        """Owned particles (sorted order when nranks == 1, unspecified otherwise) with the last outputs."""
         dev = self.device
-        f = [torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(8)]
-        ids = torch.empty(self.n, dtype=torch.int32, device=dev)
+        n = self.n if self.nranks == 1 else self.stats(check=False)["n_owned"]
+        f = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(8)]
+        ids = torch.empty(n, dtype=torch.int32, device=dev)
         x, y, z, q, phi, fx, fy, fz = f
         self._check(self._lib.pi_get_particles(self._h, _ptr(x), _ptr(y), _ptr(z), _ptr(q), _ptr(ids), _ptr(phi),
                                                _ptr(fx), _ptr(fy), _ptr(fz)))

@@ -41,6 +41,8 @@ P = ctypes.c_void_p
 SIGNATURES = {
     "pi_abi_version": (ctypes.c_int32, []),
     "pi_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(pi_config)]),
+    "pi_slab_info": (ctypes.c_int, [ctypes.POINTER(pi_config), ctypes.POINTER(ctypes.c_int64)]),
+    "pi_nccl_unique_id": (ctypes.c_int, [P]),
     "pi_create": (ctypes.c_int, [ctypes.POINTER(pi_config), P, ctypes.c_size_t, ctypes.POINTER(P)]),
     "pi_destroy": (ctypes.c_int, [P]),
     "pi_set_stream": (ctypes.c_int, [P, P]),

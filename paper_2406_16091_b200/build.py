@@ -54,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     vs = os.path.join(objdir, "exports.map")
     with open(vs, "w") as f:
         f.write("{ global: pi_*; local: *; };\n")
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xlinker", "--version-script=" + vs]
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xlinker", "--version-script=" + vs, "-ldl", "-lpthread"]
     subprocess.check_call(cmd)
     return LIB
 

@@ -1,12 +1,13 @@
 // C ABI of libpi (include/pi.h): context, workspace carving, call sequencing.
 #include <cmath>
-#include <cstddef>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <new>
 
 #include "pi_internal.cuh"
+#include "slab.cuh"
 
 using namespace pi;
 
@@ -17,10 +18,45 @@ constexpr size_t ALIGN = 256;
 size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-  size_t ctl, counts, offsets, tiles, rec, sid, perm, urec, uid, rank, outs, io, total;
+  size_t ctl, counts, offsets, tiles, rec, sid, perm, urec, uid, rank, outs, io;
+  size_t xrec, xid, xperm, msg[4];  // nranks > 1
+  size_t total;
 };
 
-Layout make_layout(long long ncells, long long cap) {
+// Decomposition of cfg: local X layers and the fixed message capacity (nranks > 1).
+struct SlabGeom {
+  int Lx, nx_local, gx_off, own_lo, own_hi;
+  long long ncells_local, cap_msg;
+};
+
+SlabGeom slab_geom(const pi_config *cfg) {
+  SlabGeom s{};
+  const int P = cfg->nranks;
+  s.Lx = cfg->dims[0] / P;
+  if (P > 1) {
+    s.nx_local = s.Lx + 2;            // ghost layers at local 0 and Lx + 1
+    s.gx_off = cfg->rank * s.Lx - 1;  // global X cell of local cell 0
+    s.own_lo = 1;
+    s.own_hi = s.Lx + 1;
+    // a boundary X layer holds ~capacity / (Lx + 2) particles; 2.5x covers its fluctuation
+    // and the migrants of one step (|dx| < w), with a floor for tiny slabs
+    const long long cap = cfg->capacity > 0 ? cfg->capacity : 1;
+    s.cap_msg = (long long)(2.5 * (double)cap / s.nx_local) + 1024;
+  } else {
+    s.nx_local = cfg->dims[0];
+    s.gx_off = 0;
+    s.own_lo = 0;
+    s.own_hi = cfg->dims[0];
+    s.cap_msg = 0;
+  }
+  s.ncells_local = (long long)s.nx_local * cfg->dims[1] * cfg->dims[2];
+  return s;
+}
+
+Layout make_layout(const pi_config *cfg) {
+  const SlabGeom sg = slab_geom(cfg);
+  const long long ncells = sg.ncells_local;
+  const long long cap = cfg->capacity > 0 ? cfg->capacity : 1;
   Layout L{};
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -40,6 +76,12 @@ Layout make_layout(long long ncells, long long cap) {
   L.rank = take(sizeof(int32_t) * (size_t)cap);
   L.outs = take(sizeof(float4) * (size_t)cap);
   L.io = take(sizeof(float) * 8 * (size_t)cap);
+  if (cfg->nranks > 1) {
+    L.xrec = take(sizeof(float4) * (size_t)cap);
+    L.xid = take(sizeof(int32_t) * (size_t)cap);
+    L.xperm = take(sizeof(int32_t) * (size_t)cap);
+    for (int k = 0; k < 4; ++k) L.msg[k] = take(msg_bytes(sg.cap_msg));
+  }
   L.total = o;
   return L;
 }
@@ -67,18 +109,20 @@ __global__ void k_unpack(long long n, const float4 *__restrict__ rec, const int3
   }
 }
 
-__global__ void k_binning_export(long long n, long long ncells, const float4 *__restrict__ rec,
+__global__ void k_binning_export(long long n, const long long *n_dev, long long ncells, const float4 *__restrict__ rec,
                                  const int32_t *__restrict__ perm, const int32_t *__restrict__ offsets, Geom g,
                                  int32_t *cell_of, int32_t *counts, int32_t *offs_out, int32_t *perm_out) {
+  if (n_dev) n = *n_dev;
   long long stride = (long long)gridDim.x * blockDim.x;
   long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   for (long long i = t0; i < n; i += stride) {
-    if (cell_of) {
+    const int pi_ = perm[i];
+    if (cell_of && pi_ >= 0) {
       bool bad = false;
       float4 r = rec[i];
-      cell_of[perm[i]] = cell_lin(g, r.x, r.y, r.z, bad);
+      cell_of[pi_] = cell_lin(g, r.x, r.y, r.z, bad);
     }
-    if (perm_out) perm_out[i] = perm[i];
+    if (perm_out) perm_out[i] = pi_;
   }
   for (long long c = t0; c <= ncells; c += stride) {
     if (offs_out) offs_out[c] = offsets[c];
@@ -107,11 +151,12 @@ struct pi_ctx_s {
   unsigned long long *tiles;
   float4 *rec, *urec, *outs;
   float *io;
-  long long n;       // owned particles
-  int state;         // 0 empty, 1 binned from pi_bin, 2 sorted state from pi_step (U pending)
-  bool need_bin;     // pi_step must re-bin U first
+  long long n;       // owned particles (exact on the host when nranks == 1; pi_bin's n otherwise)
+  int state;         // 0 empty, 1 binned from pi_bin, 2 sorted state from pi_step (update pending)
+  bool need_bin;     // pi_step must re-bin (and, nranks > 1, migrate) first
   bool interacted;
   long long steps;
+  SlabState slab;    // nranks > 1
   cudaEvent_t ev[4][2];  // phase timing: 0 bin, 1 interact, 2 exchange, 3 host copies
   bool ev_used[4];
   char err[512];
@@ -149,7 +194,7 @@ static bool config_ok(const pi_config *cfg, char *why, size_t n) {
   if (cfg->capacity < 0 || cfg->capacity > (1LL << 31) - 64) { snprintf(why, n, "capacity out of range"); return false; }
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) { snprintf(why, n, "bad rank/nranks"); return false; }
   if (cfg->dims[0] % cfg->nranks) { snprintf(why, n, "dims[0] must be divisible by nranks"); return false; }
-  if (cfg->nranks > 1) { snprintf(why, n, "nranks > 1 requires the multi-GPU build (pi_mgpu)"); return false; }
+  if (cfg->nranks > 1 && !cfg->nccl_unique_id) { snprintf(why, n, "nranks > 1 needs nccl_unique_id"); return false; }
   long long nc = (long long)cfg->dims[0] * cfg->dims[1] * cfg->dims[2];
   if (nc > (1LL << 30)) { snprintf(why, n, "too many cells"); return false; }
   return true;
@@ -162,8 +207,28 @@ int32_t pi_abi_version(void) { return PI_ABI_VERSION; }
 size_t pi_workspace_bytes(const pi_config *cfg) {
   char why[256];
   if (!config_ok(cfg, why, sizeof(why))) return 0;
-  long long nc = (long long)cfg->dims[0] * cfg->dims[1] * cfg->dims[2];
-  return make_layout(nc, cfg->capacity > 0 ? cfg->capacity : 1).total;
+  return make_layout(cfg).total;
+}
+
+pi_status pi_slab_info(const pi_config *cfg, int64_t out[8]) {
+  char why[256];
+  if (!out || !config_ok(cfg, why, sizeof(why))) return PI_EINVAL;
+  const SlabGeom s = slab_geom(cfg);
+  out[0] = s.Lx;
+  out[1] = (int64_t)cfg->rank * s.Lx;        // first owned global X cell
+  out[2] = (int64_t)(cfg->rank + 1) * s.Lx;  // one past the last
+  out[3] = s.nx_local;
+  out[4] = s.gx_off;
+  out[5] = s.own_lo;
+  out[6] = s.own_hi;
+  out[7] = s.cap_msg;
+  return PI_OK;
+}
+
+pi_status pi_nccl_unique_id(void *out128) {
+  char why[256];
+  if (!out128) return PI_EINVAL;
+  return nccl_unique_id(out128, why, sizeof(why)) ? PI_OK : PI_ENCCL;
 }
 
 pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_ctx *out) {
@@ -171,8 +236,8 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   if (!out) return PI_EINVAL;
   *out = nullptr;
   if (!config_ok(cfg, why, sizeof(why))) return PI_EINVAL;
-  long long nc = (long long)cfg->dims[0] * cfg->dims[1] * cfg->dims[2];
-  Layout lay = make_layout(nc, cfg->capacity > 0 ? cfg->capacity : 1);
+  const SlabGeom sg = slab_geom(cfg);
+  Layout lay = make_layout(cfg);
   if (!workspace || ws_bytes < lay.total || (reinterpret_cast<uintptr_t>(workspace) & (ALIGN - 1))) return PI_EINVAL;
   pi_ctx c = new (std::nothrow) pi_ctx_s();
   if (!c) return PI_EINVAL;
@@ -193,15 +258,19 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   c->rank = reinterpret_cast<int32_t *>(c->ws + lay.rank);
   c->outs = reinterpret_cast<float4 *>(c->ws + lay.outs);
   c->io = reinterpret_cast<float *>(c->ws + lay.io);
-  // geometry (one rank: local grid == global grid)
+  // geometry: the cell contract is evaluated on the GLOBAL grid, the local grid is the slab
   Geom &g = c->g;
   g.ox = cfg->origin[0]; g.oy = cfg->origin[1]; g.oz = cfg->origin[2];
   g.w = cfg->cell_width;
   g.inv_w = 1.0f / cfg->cell_width;  // contract C3: fl32(1/w), IEEE division on the host
-  g.nx = cfg->dims[0]; g.ny = cfg->dims[1]; g.nz = cfg->dims[2];
-  g.ncells = nc;
+  g.nx = sg.nx_local; g.ny = cfg->dims[1]; g.nz = cfg->dims[2];
+  g.ncells = sg.ncells_local;
+  g.gnx = cfg->dims[0];
+  g.gx_off = sg.gx_off;
+  g.own_lo = sg.own_lo;
+  g.own_hi = sg.own_hi;
   g.lx = g.ox; g.ly = g.oy; g.lz = g.oz;
-  g.hx = g.ox + (float)g.nx * g.w;
+  g.hx = g.ox + (float)cfg->dims[0] * g.w;
   g.hy = g.oy + (float)g.ny * g.w;
   g.hz = g.oz + (float)g.nz * g.w;
   KParams &k = c->kp;
@@ -221,24 +290,50 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
     delete c;
     return s;
   }
-  for (int k = 0; k < 4; ++k)
+  for (int kk = 0; kk < 4; ++kk)
     for (int b = 0; b < 2; ++b) {
-      e = cudaEventCreate(&c->ev[k][b]);
+      e = cudaEventCreate(&c->ev[kk][b]);
       if (e != cudaSuccess) {
         pi_status s = cuda_check(c, e, "pi_create events");
         pi_destroy(c);
         return s;
       }
     }
+  if (cfg->nranks > 1) {
+    SlabState &S = c->slab;
+    S.rank = cfg->rank;
+    S.nranks = cfg->nranks;
+    S.Lx = sg.Lx;
+    S.cap_msg = sg.cap_msg;
+    S.sendL = c->ws + lay.msg[0];
+    S.sendR = c->ws + lay.msg[1];
+    S.recvL = c->ws + lay.msg[2];
+    S.recvR = c->ws + lay.msg[3];
+    S.xrec = reinterpret_cast<float4 *>(c->ws + lay.xrec);
+    S.xid = reinterpret_cast<int32_t *>(c->ws + lay.xid);
+    S.xperm = reinterpret_cast<int32_t *>(c->ws + lay.xperm);
+    if ((e = cudaMemsetAsync(c->ws + lay.msg[0], 0, lay.total - lay.msg[0], c->stream)) != cudaSuccess) {
+      pi_status s = cuda_check(c, e, "pi_create memset msgs");
+      pi_destroy(c);
+      return s;
+    }
+    S.tr = make_transport(cfg, &S, c->err, sizeof(c->err));
+    if (!S.tr) {
+      pi_destroy(c);
+      return PI_ENCCL;
+    }
+  }
   *out = c;
   return PI_OK;
 }
 
 pi_status pi_destroy(pi_ctx c) {
-  if (c)
+  if (c) {
     for (int k = 0; k < 4; ++k)
       for (int b = 0; b < 2; ++b)
         if (c->ev[k][b]) cudaEventDestroy(c->ev[k][b]);
+    delete c->slab.tr;
+  }
   delete c;
   return PI_OK;
 }
@@ -255,10 +350,12 @@ pi_status pi_set_tuning(pi_ctx c, const pi_tuning *t) {
   return PI_OK;
 }
 
+// a1-a4 on SoA input (x != NULL) or on AoS records.
 static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, const float *z, const float *q,
-                        const int32_t *id, const float4 *rec_in) {
+                        const int32_t *id, const float4 *rec_in, const int32_t *perm_in, const long long *n_dev) {
   BinArgs a{};
   a.n = n;
+  a.n_dev = n_dev;
   a.x = x; a.y = y; a.z = z; a.q = q;
   a.rec_in = rec_in;
   a.id_in = id;
@@ -269,12 +366,30 @@ static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, c
   a.tile_status = c->tiles;
   a.rec_out = c->rec;
   a.sid_out = c->sid;
-  a.perm_out = rec_in ? nullptr : c->perm;
+  a.perm_out = (rec_in && !perm_in) ? nullptr : c->perm;
+  a.perm_in = perm_in;
   a.ctl = c->ctl;
   phase_begin(c, 0);
   cudaError_t e = launch_bin(c->g, a, c->stream);
   phase_end(c, 0);
   return cuda_check(c, e, "pi_bin");
+}
+
+// a8: exchange the first / last owned X layers as ghosts, append them, bin owned + ghosts.
+static pi_status slab_ghosts_and_bin(pi_ctx c) {
+  SlabState &S = c->slab;
+  const long long cap = c->cfg.capacity;
+  cudaError_t e;
+  phase_begin(c, 2);
+  if ((e = slab_reset(S, c->ctl, c->stream)) != cudaSuccess) return cuda_check(c, e, "slab reset");
+  if ((e = slab_select_ghosts(S, c->g, cap, c->ctl, c->stream)) != cudaSuccess) return cuda_check(c, e, "ghosts");
+  if ((e = S.tr->exchange(S, c->stream)) != cudaSuccess) return fail(c, PI_ENCCL, "ghost exchange failed");
+  if ((e = slab_append(S, &c->ctl->n_owned, &c->ctl->n_total, &c->ctl->ghosts_in, &c->ctl->pad2[1], cap, c->ctl,
+                       c->stream)) !=
+      cudaSuccess)
+    return cuda_check(c, e, "ghost append");
+  phase_end(c, 2);
+  return do_bin(c, cap, nullptr, nullptr, nullptr, nullptr, S.xid, S.xrec, S.xperm, &c->ctl->n_total);
 }
 
 pi_status pi_bin(pi_ctx c, int64_t n, const float *x, const float *y, const float *z, const float *q,
@@ -286,7 +401,14 @@ pi_status pi_bin(pi_ctx c, int64_t n, const float *x, const float *y, const floa
   if (n > 0 && (!x || !y || !z || !q)) return fail(c, PI_EINVAL, "NULL position/value pointer");
   if (n > 0 && (!aligned16(x) || !aligned16(y) || !aligned16(z) || !aligned16(q)))
     return fail(c, PI_EINVAL, "x, y, z, q must be 16-byte aligned");
-  pi_status s = do_bin(c, n, x, y, z, q, id, nullptr);
+  pi_status s;
+  if (c->cfg.nranks > 1) {
+    cudaError_t e = slab_from_soa(c->slab, c->g, n, x, y, z, q, id, c->ctl, c->stream);
+    if (e != cudaSuccess) return cuda_check(c, e, "pi_bin slab input");
+    s = slab_ghosts_and_bin(c);
+  } else {
+    s = do_bin(c, n, x, y, z, q, id, nullptr, nullptr, nullptr);
+  }
   if (s != PI_OK) return s;
   c->n = n;
   c->state = 1;
@@ -298,7 +420,10 @@ pi_status pi_bin(pi_ctx c, int64_t n, const float *x, const float *y, const floa
 static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, float *fy, float *fz, bool integrate,
                              float dt) {
   InteractArgs a{};
-  a.n = c->n;
+  const bool multi = c->cfg.nranks > 1;
+  a.n = multi ? c->cfg.capacity : c->n;
+  a.n_dev = multi ? &c->ctl->n_total : nullptr;
+  a.n_est = multi ? c->n * (long long)(c->slab.Lx + 2) / (c->slab.Lx > 0 ? c->slab.Lx : 1) : c->n;
   a.rec = c->rec;
   a.offsets = c->offsets;
   a.ctl = c->ctl;
@@ -347,7 +472,26 @@ pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
   if (c->state == 0) return fail(c, PI_ESTATE, "pi_step before pi_bin");
   if (!std::isfinite(dt)) return fail(c, PI_EINVAL, "dt must be finite");
   if (c->need_bin) {
-    pi_status s = do_bin(c, c->n, nullptr, nullptr, nullptr, nullptr, c->uid, c->urec);
+    pi_status s;
+    if (c->cfg.nranks > 1) {
+      // a8: migration of the particles whose updated cell left the slab, then ghosts + bin
+      SlabState &S = c->slab;
+      const long long cap = c->cfg.capacity;
+      cudaError_t e;
+      phase_begin(c, 2);
+      if ((e = slab_reset(S, c->ctl, c->stream)) != cudaSuccess) return cuda_check(c, e, "slab reset");
+      if ((e = slab_migrate(S, c->g, cap, c->rec, c->urec, c->uid, c->ctl, c->stream)) != cudaSuccess)
+        return cuda_check(c, e, "migrate");
+      if ((e = S.tr->exchange(S, c->stream)) != cudaSuccess) return fail(c, PI_ENCCL, "migration exchange failed");
+      if ((e = slab_append(S, &c->ctl->n_stay, &c->ctl->n_owned, &c->ctl->migrants_in, &c->ctl->migrants_out, cap,
+                           c->ctl, c->stream)) !=
+          cudaSuccess)
+        return cuda_check(c, e, "migrant append");
+      phase_end(c, 2);
+      s = slab_ghosts_and_bin(c);
+    } else {
+      s = do_bin(c, c->n, nullptr, nullptr, nullptr, nullptr, c->uid, c->urec, nullptr, nullptr);
+    }
     if (s != PI_OK) return s;
   }
   pi_status s = do_interact(c, algo, nullptr, nullptr, nullptr, nullptr, true, dt);
@@ -394,9 +538,11 @@ pi_status pi_get_binning(pi_ctx c, int32_t *cell_of, int32_t *counts, int32_t *o
   if (c->state == 0) return fail(c, PI_ESTATE, "no binning yet");
   if (c->need_bin && (cell_of || perm)) return fail(c, PI_ESTATE, "binning superseded by pi_step");
   if (c->state != 1 && (cell_of || perm)) return fail(c, PI_ESTATE, "cell_of/perm refer to a pi_bin input");
-  long long n = c->n;
+  const bool multi = c->cfg.nranks > 1;
+  long long n = multi ? c->cfg.capacity : c->n;
   long long work = n > c->g.ncells + 1 ? n : c->g.ncells + 1;
-  k_binning_export<<<blocks_for(work, 256), 256, 0, c->stream>>>(n, c->g.ncells, c->rec, c->perm, c->offsets, c->g,
+  k_binning_export<<<blocks_for(work, 256), 256, 0, c->stream>>>(n, multi ? &c->ctl->n_total : nullptr,
+                                                                 c->g.ncells, c->rec, c->perm, c->offsets, c->g,
                                                                  cell_of, counts, offsets, perm);
   return cuda_check(c, cudaGetLastError(), "pi_get_binning");
 }
@@ -407,6 +553,12 @@ pi_status pi_get_particles(pi_ctx c, float *x, float *y, float *z, float *q, int
   if (c->state == 0) return fail(c, PI_ESTATE, "no particles yet");
   const float4 *rec = c->need_bin ? c->urec : c->rec;
   const int32_t *ids = c->need_bin ? c->uid : c->sid;
+  if (c->cfg.nranks > 1) {
+    // owned particles only (ghost slots are skipped), in an arbitrary order; count in pi_stats
+    cudaError_t e = slab_export_owned(c->g, c->cfg.capacity, c->rec, rec, ids, c->interacted ? c->outs : nullptr,
+                                      x, y, z, q, id, phi, fx, fy, fz, c->ctl, c->stream);
+    return cuda_check(c, e, "pi_get_particles");
+  }
   if (c->n > 0)
     k_unpack<<<blocks_for(c->n, 256), 256, 0, c->stream>>>(c->n, rec, ids, c->interacted ? c->outs : nullptr, x, y,
                                                            z, q, id, phi, fx, fy, fz);
@@ -420,8 +572,15 @@ pi_status pi_get_stats(pi_ctx c, pi_stats *out) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_check(c, e, "pi_get_stats");
   memset(out, 0, sizeof(*out));
-  out->n_owned = c->n;
-  out->n_ghost = 0;
+  if (c->cfg.nranks > 1) {
+    out->n_owned = h.n_owned;
+    out->n_ghost = h.n_total - h.n_owned;
+    out->migrants_in = h.migrants_in;
+    out->migrants_out = h.migrants_out;
+  } else {
+    out->n_owned = c->n;
+    out->n_ghost = 0;
+  }
   out->max_per_cell = h.max_per_cell;
   out->flags = h.flags;
   unsigned long long cand = 0;

@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_count_soa(long long n, const 
 // a1 + a2 over AoS records (pi_step re-binning of the updated sorted state).
 __global__ void __launch_bounds__(COUNT_THREADS) k_count_aos(long long n, const float4 *__restrict__ rec, Geom g,
                                                               int32_t *__restrict__ counts,
-                                                              int32_t *__restrict__ rank, DevCtl *ctl) {
+                                                              int32_t *__restrict__ rank, DevCtl *ctl,
+                                                              const long long *n_dev) {
+  if (n_dev) n = *n_dev;
   bool bad = false;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -263,7 +265,10 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
                                                             const int32_t *__restrict__ offsets,
                                                             float4 *__restrict__ rec_out,
                                                             int32_t *__restrict__ sid_out,
-                                                            int32_t *__restrict__ perm_out) {
+                                                            int32_t *__restrict__ perm_out,
+                                                            const int32_t *__restrict__ perm_in,
+                                                            const long long *n_dev) {
+  if (n_dev) n = *n_dev;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     float4 r;
@@ -277,7 +282,7 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
     int slot = __ldg(offsets + lin) + __ldg(rank + i);
     rec_out[slot] = r;
     sid_out[slot] = id_in ? __ldg(id_in + i) : (int32_t)i;
-    if (perm_out) perm_out[slot] = (int32_t)i;
+    if (perm_out) perm_out[slot] = perm_in ? __ldg(perm_in + i) : (int32_t)i;
   }
 }
 
@@ -297,7 +302,7 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
   if (a.n > 0) {
     if (a.rec_in) {
       k_count_aos<<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.rec_in, g, a.counts, a.rank,
-                                                                         a.ctl);
+                                                                         a.ctl, a.n_dev);
     } else {
       k_count_soa<<<grid_for((a.n + 3) / 4, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.x, a.y, a.z, g,
                                                                                    a.counts, a.rank, a.cell_of,
@@ -310,10 +315,11 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
     if (a.rec_in)
       k_scatter<true><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
           a.n, nullptr, nullptr, nullptr, nullptr, a.rec_in, a.id_in, g, a.rank, a.offsets, a.rec_out, a.sid_out,
-          a.perm_out);
+          a.perm_out, a.perm_in, a.n_dev);
     else
       k_scatter<false><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
-          a.n, a.x, a.y, a.z, a.q, nullptr, a.id_in, g, a.rank, a.offsets, a.rec_out, a.sid_out, a.perm_out);
+          a.n, a.x, a.y, a.z, a.q, nullptr, a.id_in, g, a.rank, a.offsets, a.rec_out, a.sid_out, a.perm_out, nullptr,
+          nullptr);
   }
   return cudaGetLastError();
 }

@@ -109,8 +109,8 @@ __global__ void __launch_bounds__(NT) k_interact_fullload(FlParams p) {
 
   const Geom &g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int x0 = blockIdx.x * bx, y0 = blockIdx.y * by, z0 = blockIdx.z * bz;
-  const int ex = min(bx, g.nx - x0), ey = min(by, g.ny - y0), ez = min(bz, g.nz - z0);  // interior extent
+  const int x0 = g.own_lo + blockIdx.x * bx, y0 = blockIdx.y * by, z0 = blockIdx.z * bz;  // owned cells only
+  const int ex = min(bx, g.own_hi - x0), ey = min(by, g.ny - y0), ez = min(bz, g.nz - z0);  // interior extent
   const float thr = p.kp.rc2, mc2 = -p.kp.c2;
   unsigned long long cand = 0;
 
@@ -262,7 +262,8 @@ cudaError_t launch_k(const FlParams &p, cudaStream_t s) {
   cudaError_t e =
       cudaFuncSetAttribute(k_interact_fullload<KERNEL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((p.g.nx + p.bx - 1) / p.bx, (p.g.ny + p.by - 1) / p.by, (p.g.nz + p.bz - 1) / p.bz);
+  const int own = p.g.own_hi - p.g.own_lo;
+  dim3 grid((own + p.bx - 1) / p.bx, (p.g.ny + p.by - 1) / p.by, (p.g.nz + p.bz - 1) / p.bz);
   k_interact_fullload<KERNEL, NT><<<grid, NT, smem, s>>>(p);
   return cudaGetLastError();
 }
@@ -291,12 +292,12 @@ cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const Inte
   p.bx = a.fb[0] > 0 ? a.fb[0] : 8;
   p.by = a.fb[1] > 0 ? a.fb[1] : 4;
   p.bz = a.fb[2] > 0 ? a.fb[2] : 4;
-  p.bx = min(p.bx, g.nx);
+  p.bx = min(p.bx, g.own_hi - g.own_lo);
   p.by = min(p.by, g.ny);
   p.bz = min(p.bz, g.nz);
   // fewer than 27 staged cells cannot hold one target cell and its ghosts;
   // with the ghost shell always included here the smallest box is 1x1x1 (+ shell = 27 cells)
-  const double ppc = (double)a.n / (double)g.ncells;
+  const double ppc = (double)a.n_est / (double)g.ncells;
   const double staged = (double)(p.bx + 2) * (p.by + 2) * (p.bz + 2);
   p.cap = a.fb_cap > 0 ? a.fb_cap : (int)(staged * ppc * 1.25 + 64.0);
   p.cap = (p.cap + 31) & ~31;

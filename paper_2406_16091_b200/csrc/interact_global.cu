@@ -18,13 +18,22 @@ constexpr int PPNL_THREADS = 128;
 template <int KERNEL>
 __global__ void __launch_bounds__(PPNL_THREADS) k_interact_global(long long n, const float4 *__restrict__ rec,
                                                                   const int32_t *__restrict__ offsets, Geom g,
-                                                                  KParams kp, OutDesc out, DevCtl *ctl) {
+                                                                  KParams kp, OutDesc out, DevCtl *ctl,
+                                                                  const long long *n_dev) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long cand = 0;
+  if (n_dev) n = *n_dev;
+  bool owned = false;
+  float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
+  int cx = 0;
   if (t < n) {
-    const float4 me = __ldg(rec + t);
+    me = __ldg(rec + t);
     bool bad = false;
-    const int cx = cell_coord(me.x, g.ox, g.inv_w, g.nx, bad);
+    cx = cell_x(g, me.x, bad);
+    owned = cx >= g.own_lo && cx < g.own_hi;  // ghost particles are sources only
+  }
+  if (owned) {
+    bool bad = false;
     const int cy = cell_coord(me.y, g.oy, g.inv_w, g.ny, bad);
     const int cz = cell_coord(me.z, g.oz, g.inv_w, g.nz, bad);
     const int xlo = max(cx - 1, 0), xhi = min(cx + 1, g.nx - 1);
@@ -81,13 +90,16 @@ cudaError_t launch_interact_global(const Geom &g, const KParams &k, const Intera
   int blocks = (int)((a.n + PPNL_THREADS - 1) / PPNL_THREADS);
   switch (k.kernel) {
     case PI_K_GAUSSIAN:
-      k_interact_global<PI_K_GAUSSIAN><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl);
+      k_interact_global<PI_K_GAUSSIAN><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl,
+                                                                        a.n_dev);
       break;
     case PI_K_INDICATOR:
-      k_interact_global<PI_K_INDICATOR><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl);
+      k_interact_global<PI_K_INDICATOR><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl,
+                                                                         a.n_dev);
       break;
     default:
-      k_interact_global<PI_K_CANDIDATE><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl);
+      k_interact_global<PI_K_CANDIDATE><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl,
+                                                                         a.n_dev);
   }
   return cudaGetLastError();
 }

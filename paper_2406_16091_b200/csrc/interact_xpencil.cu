@@ -110,8 +110,8 @@ __device__ void build_tables(const XpParams &p, const Slot &sl, long long item, 
   const long long row = item / p.nseg;
   cy = (int)(row % g.ny);
   cz = (int)(row / g.ny);
-  x0 = seg * L;
-  Lseg = min(L, g.nx - x0);
+  x0 = g.own_lo + seg * L;  // owned X cells only (ghost layers are staged as sources)
+  Lseg = min(L, g.own_hi - x0);
   // offsets of the 9 neighbour rows over cells x0-1 .. x0+L+1: all loads issued first
   constexpr int MAXK = (9 * 67 + 31) / 32;
   int v[MAXK];
@@ -439,10 +439,11 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   p.kp = k;
   p.out = a.out;
   p.ctl = a.ctl;
+  const int own = g.own_hi - g.own_lo;
   p.L = a.tx_len > 0 ? a.tx_len : 32;
   if (p.L > 64) p.L = 64;
-  if (p.L > g.nx) p.L = g.nx;
-  p.nseg = (g.nx + p.L - 1) / p.L;
+  if (p.L > own) p.L = own;
+  p.nseg = (own + p.L - 1) / p.L;
   p.nitems = (long long)p.nseg * g.ny * g.nz;
   // consumer warps (threads = 32 * NC target threads + one producer warp)
   const int nc = a.threads == 512 ? 16 : (a.threads == 128 ? 4 : 8);
@@ -450,7 +451,7 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
     p.cap = a.tx_cap;
   } else {
     // mean occupancy of 9 rows x (L + 2) cells (+ 10 %), plus the padding (< 8 per cell)
-    const double ppc = (double)a.n / (double)g.ncells;
+    const double ppc = (double)a.n_est / (double)g.ncells;
     p.cap = (int)((9.0 * ppc * 1.1 + 4.0) * (p.L + 2) + 128.0);
   }
   p.cap = (p.cap + 31) & ~31;

@@ -11,11 +11,14 @@ namespace pi {
 // Geometry and kernel constants, passed by value to every kernel.
 // ------------------------------------------------------------------------------------
 struct Geom {
-  float ox, oy, oz;   // origin of the LOCAL grid (== global unless nranks > 1)
+  float ox, oy, oz;   // origin of the GLOBAL grid (the cell contract is evaluated globally)
   float w, inv_w;     // cell width and fl32(1/w) (contract C3)
-  int nx, ny, nz;     // local grid dims
-  long long ncells;
-  float hx, hy, hz;   // upper faces of the box this rank owns (integration walls)
+  int nx, ny, nz;     // LOCAL grid dims (nx = owned X layers + 2 ghost layers when nranks > 1)
+  long long ncells;   // local cells
+  int gnx;            // global dims[0]
+  int gx_off;         // global X index of local X cell 0 (-1 + rank * Lx when nranks > 1)
+  int own_lo, own_hi; // owned local X cells [own_lo, own_hi): targets of the interaction
+  float hx, hy, hz;   // upper faces of the global box (integration walls)
   float lx, ly, lz;   // lower faces
 };
 
@@ -36,6 +39,12 @@ struct DevCtl {
   int max_per_cell;      // M_C of the last scan
   int flags;             // sticky error bits
   int pad0;
+  // X-slab state (nranks > 1), device resident so no host synchronisation is needed
+  long long n_owned, n_total;         // owned particles; owned + ghost particles (binned)
+  long long n_stay;                   // stayers after the position update (migration)
+  long long migrants_in, migrants_out, ghosts_in;
+  long long pad2[2];
+  // everything from here on is reset before each interaction
   unsigned long long fallback_cells;
   unsigned long long xp_items;        // X-pencil work-item counter (reset before each launch)
   unsigned long long pad[2];
@@ -43,7 +52,7 @@ struct DevCtl {
 };
 constexpr int CAND_SLOTS = 64;
 
-enum : int { FLAG_OUT_OF_BOX = 1, FLAG_CAPACITY = 2, FLAG_INTERNAL = 4 };
+enum : int { FLAG_OUT_OF_BOX = 1, FLAG_CAPACITY = 2, FLAG_INTERNAL = 4, FLAG_DOMAIN = 8 };
 
 // ------------------------------------------------------------------------------------
 // a1: cell index, contract C3: c = clamp(floor(fl32(fl32(x - o) * inv_w)), 0, N - 1).
@@ -58,8 +67,14 @@ __device__ __forceinline__ int cell_coord(float x, float o, float inv_w, int nd,
   return c;
 }
 
+// Local X cell: the global contract, then the slab offset (clamped into the local grid).
+__device__ __forceinline__ int cell_x(const Geom &g, float x, bool &bad) {
+  const int c = cell_coord(x, g.ox, g.inv_w, g.gnx, bad) - g.gx_off;
+  return min(max(c, 0), g.nx - 1);
+}
+
 __device__ __forceinline__ int cell_lin(const Geom &g, float x, float y, float z, bool &bad) {
-  int cx = cell_coord(x, g.ox, g.inv_w, g.nx, bad);
+  int cx = cell_x(g, x, bad);
   int cy = cell_coord(y, g.oy, g.inv_w, g.ny, bad);
   int cz = cell_coord(z, g.oz, g.inv_w, g.nz, bad);
   return cx + g.nx * (cy + g.ny * cz);
@@ -105,11 +120,13 @@ __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, in
                                              float fx, float fy, float fz) {
   o.sorted[t] = make_float4(phi, fx, fy, fz);
   if (o.perm) {
-    int c = o.perm[t];
-    if (o.phi) o.phi[c] = phi;
-    if (o.fx) o.fx[c] = fx;
-    if (o.fy) o.fy[c] = fy;
-    if (o.fz) o.fz[c] = fz;
+    const int c = o.perm[t];
+    if (c >= 0) {  // -1: not a particle of the caller's pi_bin input (ghost)
+      if (o.phi) o.phi[c] = phi;
+      if (o.fx) o.fx[c] = fx;
+      if (o.fy) o.fy[c] = fy;
+      if (o.fz) o.fz[c] = fz;
+    }
   }
   if (o.upd) {
     float4 u;
@@ -126,7 +143,8 @@ __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, in
 // Launchers (host side, in the .cu files).
 // ------------------------------------------------------------------------------------
 struct BinArgs {
-  long long n;
+  long long n;                  // particles (upper bound when n_dev is set)
+  const long long *n_dev;       // device-resident count (nranks > 1), or NULL
   const float *x, *y, *z, *q;   // SoA input (pi_bin), or NULL when rec_in is used
   const float4 *rec_in;         // AoS input (pi_step re-binning)
   const int32_t *id_in;         // ids (NULL -> index)
@@ -139,6 +157,7 @@ struct BinArgs {
   float4 *rec_out;              // sorted records (x, y, z, q)
   int32_t *sid_out;             // sorted ids
   int32_t *perm_out;            // sorted slot -> input index (nullable)
+  const int32_t *perm_in;       // AoS path: input index per record (-1 = ghost), or NULL
   DevCtl *ctl;
 };
 
@@ -146,7 +165,9 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s);
 int scan_tiles(long long ncells);
 
 struct InteractArgs {
-  long long n;                  // particles in the sorted state
+  long long n;                  // particles in the sorted state (upper bound if n_dev)
+  const long long *n_dev;       // device-resident count (nranks > 1), or NULL
+  long long n_est;              // host estimate of the sorted count (sizes staging buffers)
   const float4 *rec;            // sorted records
   const int32_t *offsets;       // [ncells + 1]
   OutDesc out;

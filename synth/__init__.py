@@ -205,3 +205,29 @@ def scaled_uniform(ppc: float, dims: tuple, seed: int, qkind: str = "pos") -> Cl
     grid = Grid(dims=tuple(int(d) for d in dims), w=1.0 / inv)
     n = int(round(ppc * grid.ncells))
     return uniform(n, grid, seed, qkind=qkind)
+
+
+def slab_uniform(ppc: float, slab_dims: tuple, rank: int, nranks: int, seed: int, qkind: str = "pos") -> Cloud:
+    """Rank `rank`'s share of a weak-scaling X-slab workload: the global grid is
+    (slab_dims[0] * nranks, slab_dims[1], slab_dims[2]) cells of width w = 2^-ceil(log2(max(slab_dims))),
+    and this rank draws ~ppc particles per cell uniformly inside its own slab
+    [rank * Lx * w, (rank + 1) * Lx * w) (independent stream per rank, so the union is a uniform cloud).
+    w is a power of two, so the slab faces are exact in fp32 and every particle's cell lies in the slab."""
+    lx, ny, nz = (int(d) for d in slab_dims)
+    m = max(lx, ny, nz)
+    w = 1.0 / (1 << int(math.ceil(math.log2(m))))
+    grid = Grid(dims=(lx * nranks, ny, nz), w=w)
+    n = int(round(ppc * lx * ny * nz))
+    rng = _rng(seed + 7919 * rank)
+    u = rng.random((3, n))
+    lo, hi = rank * lx * w, (rank + 1) * lx * w
+    ext = grid.extent
+
+    def place(v, a, b):
+        return np.clip((a + v * (b - a)).astype(np.float32), np.float32(a), np.nextafter(np.float32(b), np.float32(0)))
+
+    x = place(u[0], lo, hi)
+    y = place(u[1], 0.0, ext[1])
+    z = place(u[2], 0.0, ext[2])
+    q = charges(rng, n, qkind)
+    return Cloud(grid, x, y, z, q, name=f"slab{rank}of{nranks}")

@@ -1,0 +1,200 @@
+"""a8 X-slab decomposition on the GPU, through the C ABI.
+
+P contexts on ONE GPU (the round's boxes have one), linked by the library's in-process
+transport ("PILOCAL:<key>"), each driven by its own host thread as one rank per GPU would be.
+The exchange kernels (ghost selection, migration, append) and the slab-aware binning and
+interaction are the same code the NCCL transport drives; only the byte mover differs.
+Checked against the oracle on the WHOLE cloud: per-rank outputs in caller order after
+pi_bin, and forces / positions / ownership after each pi_step (migration included)."""
+import concurrent.futures as cf
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import celllist
+from oracle import reference as ref
+from tests._util import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+_key = itertools.count()
+
+
+def _contexts(g, P, capacity, kernel="gaussian"):
+    from paper_2406_16091_b200 import Context
+    uid = f"PILOCAL:test{next(_key)}".encode()
+    ctxs = []
+    for r in range(P):
+        s = torch.cuda.Stream()
+        ctxs.append(Context(g.dims, g.w, g.r_c, g.origin, kernel=kernel, sigma=0.0 if g.sigma is None else g.sigma,
+                            capacity=capacity, device="cuda", stream=s, rank=r, nranks=P, nccl_unique_id=uid))
+    return ctxs
+
+
+def _all(pool, fn, ctxs):
+    futs = [pool.submit(fn, r, c) for r, c in enumerate(ctxs)]
+    return [f.result(timeout=120) for f in futs]
+
+
+def _partition(c, ctx):
+    cx = celllist.cells(c.x, c.y, c.z, c.grid) % c.grid.dims[0]
+    idx = np.flatnonzero((cx >= ctx.slab["gx_lo"]) & (cx < ctx.slab["gx_hi"]))
+    return idx
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("algo", ["global", "xpencil", "fullload"])
+def test_slab_bin_interact_matches_whole_cloud(P, algo):
+    c = synth.make_config("c0", n=4 * 4096)
+    g = c.grid
+    ctxs = _contexts(g, P, capacity=c.n)
+    parts = [_partition(c, k) for k in ctxs]
+    assert sum(len(p) for p in parts) == c.n
+
+    def run(r, k):
+        idx = parts[r]
+        with torch.cuda.stream(k.stream):
+            k.bin(*(_dev(a[idx]) for a in (c.x, c.y, c.z, c.q)), id=_dev(idx.astype(np.int32)))
+            out = k.interact(algo)
+        k.stream.synchronize()
+        return torch.stack(out, 1).cpu().numpy().astype(np.float64), k.stats()
+
+    with cf.ThreadPoolExecutor(P) as pool:
+        res = _all(pool, run, ctxs)
+    got = np.zeros((c.n, 4))
+    for r, (out, st) in enumerate(res):
+        got[parts[r]] = out
+        assert st["n_owned"] == len(parts[r])
+        assert st["fallback_cells"] == 0 or algo == "global"
+        if 0 < r < P - 1:
+            assert st["n_ghost"] > 0
+    want = celllist.interact(c.x, c.y, c.z, c.q, g)
+    assert_parity(got, want, label=f"P={P} {algo}")
+    # candidate pairs are counted over owned targets only: their sum is the single-domain C
+    assert sum(st["candidates"] for _, st in res) == int(want["C"].sum())
+
+
+def test_slab_binning_counts_exact():
+    c = synth.make_config("c0", n=4 * 4096)
+    g = c.grid
+    P = 2
+    ctxs = _contexts(g, P, capacity=c.n)
+    parts = [_partition(c, k) for k in ctxs]
+
+    def run(r, k):
+        idx = parts[r]
+        with torch.cuda.stream(k.stream):
+            k.bin(*(_dev(a[idx]) for a in (c.x, c.y, c.z, c.q)))
+            counts, offsets = k.get_offsets()
+        k.stream.synchronize()
+        return counts.cpu().numpy(), offsets.cpu().numpy(), k.slab
+
+    with cf.ThreadPoolExecutor(P) as pool:
+        res = _all(pool, run, ctxs)
+    gcells = celllist.cells(c.x, c.y, c.z, g)
+    wc, _, _ = celllist.binning(gcells, g.ncells)
+    wc = wc.reshape(g.dims[2], g.dims[1], g.dims[0])
+    for counts, offsets, sl in res:
+        nx = sl["nx_local"]
+        loc = counts.reshape(g.dims[2], g.dims[1], nx)
+        # local X layer j holds global layer gx_off + j (owned and ghost layers alike)
+        for j in range(nx):
+            gx = sl["gx_off"] + j
+            exp = wc[:, :, gx] if 0 <= gx < g.dims[0] else np.zeros_like(loc[:, :, j])
+            assert np.array_equal(loc[:, :, j], exp), f"layer {j}"
+        assert offsets[-1] == counts.sum()
+
+
+@pytest.mark.parametrize("algo", ["xpencil", "global"])
+def test_slab_steps_migrate_and_match_oracle(algo):
+    c = synth.make_config("c0", n=4 * 4096)
+    g = c.grid
+    P = 4
+    ctxs = _contexts(g, P, capacity=c.n)
+    parts = [_partition(c, k) for k in ctxs]
+    # dt so that the fastest particle moves ~0.8 cell per step: migration every step
+    F = celllist.interact(c.x, c.y, c.z, c.q, g)["out"][:, 1:]
+    dt = float(np.float32(0.8 * g.w / np.abs(F).max()))
+
+    def bin_(r, k):
+        idx = parts[r]
+        with torch.cuda.stream(k.stream):
+            k.bin(*(_dev(a[idx]) for a in (c.x, c.y, c.z, c.q)), id=_dev(idx.astype(np.int32)))
+
+    def state(r, k):
+        with torch.cuda.stream(k.stream):
+            p = k.get_particles()
+        k.stream.synchronize()
+        return {key: v.cpu().numpy() for key, v in p.items()}, k.stats()
+
+    def step(r, k):
+        with torch.cuda.stream(k.stream):
+            k.step(algo, dt)
+
+    def union(states):
+        d = {key: np.concatenate([s[key] for s, _ in states]) for key in states[0][0]}
+        order = np.argsort(d["id"])
+        return {key: v[order] for key, v in d.items()}
+
+    ext = g.extent
+    with cf.ThreadPoolExecutor(P) as pool:
+        _all(pool, bin_, ctxs)
+        s0 = union(_all(pool, state, ctxs))
+        assert np.array_equal(s0["id"], np.arange(c.n))
+        migrated = 0
+        for it in range(3):
+            _all(pool, step, ctxs)
+            st = _all(pool, state, ctxs)
+            s1 = union(st)
+            assert np.array_equal(s1["id"], np.arange(c.n)), "a particle lost or duplicated"
+            want = celllist.interact(s0["x"], s0["y"], s0["z"], s0["q"], g)
+            got = np.stack([s1[k] for k in ("phi", "fx", "fy", "fz")], 1).astype(np.float64)
+            assert_parity(got, want, label=f"step {it}")
+            for a, ax in enumerate("xyz"):
+                exp = ref.integrate(s0[ax], got[:, a + 1], dt, 0.0, ext[a])
+                assert np.allclose(s1[ax], exp, rtol=0, atol=2e-7 + 1e-6 * dt)
+            ins = sum(s["migrants_in"] for _, s in st)
+            outs = sum(s["migrants_out"] for _, s in st)
+            assert ins == outs
+            migrated += ins
+            s0 = s1
+        assert migrated > 0
+        # the next step re-bins: every rank owns exactly the particles in its slab
+        _all(pool, step, ctxs)
+        st = _all(pool, state, ctxs)
+    cx = celllist.cells(s0["x"], s0["y"], s0["z"], g) % g.dims[0]
+    for r, (s, stats) in enumerate(st):
+        sl = ctxs[r].slab
+        want_ids = np.flatnonzero((cx >= sl["gx_lo"]) & (cx < sl["gx_hi"]))
+        assert np.array_equal(np.sort(s["id"]), want_ids)
+    for k in ctxs:
+        k.close()
+
+
+def test_slab_domain_flag():
+    """A pi_bin particle outside the rank's slab raises flag 8 (PI_EDEVICE), it is not dropped silently."""
+    from paper_2406_16091_b200 import PiError
+    c = synth.make_config("c0")
+    g = c.grid
+    ctxs = _contexts(g, 2, capacity=2 * c.n)
+
+    def run(r, k):
+        with torch.cuda.stream(k.stream):
+            k.bin(*(_dev(a) for a in (c.x, c.y, c.z, c.q)))  # the whole cloud on both ranks
+        k.stream.synchronize()
+        try:
+            k.stats()
+        except PiError as e:
+            return str(e)
+        return ""
+
+    with cf.ThreadPoolExecutor(2) as pool:
+        msgs = _all(pool, run, ctxs)
+    assert all("flags 0x8" in m for m in msgs), msgs
