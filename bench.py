@@ -303,10 +303,12 @@ def run_ours(a):
         workload = (f"X-slab weak scaling: {g.dims[0]}x{g.dims[1]}x{g.dims[2]} cells (64^3 per GPU), 8 uniform "
                     f"particles per cell (~2^21 per GPU, {int(n_all)} total), r_c = w = 1/64, Gaussian K "
                     "sigma = r_c/3, fp32; NCCL ghost + migration exchange every step")
-        launches = 10  # reset, migrate, append, reset, ghosts, append, count, scan, scatter, interact
+        # reset, migrate, append, reset, ghosts, append, count, scan, scatter (+ pairify), interact
+        launches = 10 + (1 if a.algo == "xpencil" else 0)
     else:
         workload = WORKLOAD
-        launches = 4   # count, scan, scatter, interact (+ integrate fused)
+        # count, scan, scatter, (pairify,) interact (+ integrate fused)
+        launches = 4 + (1 if a.algo == "xpencil" else 0)
     line = {
         "metric": "candidate pair interactions/s (27-cell ordered pairs) and step ms",
         "value": value,

@@ -128,12 +128,14 @@ typedef struct {
 
 /* Tuning knobs of the launch configuration (a5).  Zero fields mean "library default".   */
 typedef struct {
-  int32_t xpencil_len;       /* X-pencil: target cells per block along X                    */
-  int32_t xpencil_cap;       /* X-pencil: staged particles per round (shared memory)        */
-  int32_t fullload_box[3];   /* full load: target sub-box (interior) dims                   */
+  int32_t xpencil_len;       /* X-pencil: target cells per warp work item along X (16)      */
+  int32_t xpencil_cap;       /* X-pencil: records of one merged 9-row cell a warp stages;
+                                larger cells take the global-memory path (mean + 4.5 sd)   */
+  int32_t fullload_box[3];   /* full load: target sub-box (interior) dims (8, 4, 4)         */
   int32_t fullload_cap;      /* full load: staged particles per block                       */
   int32_t threads;           /* threads per block of the staged kernels                     */
-  int32_t lanes_per_pair;    /* staged kernels: lanes sharing one target pair (1, 2, 4)     */
+  int32_t lanes_per_target;  /* X-pencil: max lanes sharing one target (1..8; default 8,
+                                used as min(8, 32 / targets in the cell))                   */
   int32_t reserved[7];
 } pi_tuning;
 

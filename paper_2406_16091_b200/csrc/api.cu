@@ -18,7 +18,7 @@ constexpr size_t ALIGN = 256;
 size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-  size_t ctl, counts, offsets, tiles, rec, sid, perm, urec, uid, rank, outs, io;
+  size_t ctl, counts, offsets, tiles, rec, sid, perm, urec, uid, rank, outs, io, pairs;
   size_t xrec, xid, xperm, msg[4];  // nranks > 1
   size_t total;
 };
@@ -76,6 +76,7 @@ Layout make_layout(const pi_config *cfg) {
   L.rank = take(sizeof(int32_t) * (size_t)cap);
   L.outs = take(sizeof(float4) * (size_t)cap);
   L.io = take(sizeof(float) * 8 * (size_t)cap);
+  L.pairs = take(sizeof(float4) * 2 * (size_t)(cap / 2 + 1));
   if (cfg->nranks > 1) {
     L.xrec = take(sizeof(float4) * (size_t)cap);
     L.xid = take(sizeof(int32_t) * (size_t)cap);
@@ -149,7 +150,7 @@ struct pi_ctx_s {
   DevCtl *ctl;
   int32_t *counts, *offsets, *sid, *perm, *uid, *rank;
   unsigned long long *tiles;
-  float4 *rec, *urec, *outs;
+  float4 *rec, *urec, *outs, *pairs;
   float *io;
   long long n;       // owned particles (exact on the host when nranks == 1; pi_bin's n otherwise)
   int state;         // 0 empty, 1 binned from pi_bin, 2 sorted state from pi_step (update pending)
@@ -258,6 +259,7 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   c->rank = reinterpret_cast<int32_t *>(c->ws + lay.rank);
   c->outs = reinterpret_cast<float4 *>(c->ws + lay.outs);
   c->io = reinterpret_cast<float *>(c->ws + lay.io);
+  c->pairs = reinterpret_cast<float4 *>(c->ws + lay.pairs);
   // geometry: the cell contract is evaluated on the GLOBAL grid, the local grid is the slab
   Geom &g = c->g;
   g.ox = cfg->origin[0]; g.oy = cfg->origin[1]; g.oz = cfg->origin[2];
@@ -425,6 +427,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.n_dev = multi ? &c->ctl->n_total : nullptr;
   a.n_est = multi ? c->n * (long long)(c->slab.Lx + 2) / (c->slab.Lx > 0 ? c->slab.Lx : 1) : c->n;
   a.rec = c->rec;
+  a.pairs = c->pairs;
   a.offsets = c->offsets;
   a.ctl = c->ctl;
   a.out.sorted = c->outs;
@@ -437,7 +440,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.tx_len = c->tune.xpencil_len;
   a.tx_cap = c->tune.xpencil_cap;
   a.threads = c->tune.threads;
-  a.groups = c->tune.lanes_per_pair;
+  a.groups = c->tune.lanes_per_target;
   a.fb[0] = c->tune.fullload_box[0]; a.fb[1] = c->tune.fullload_box[1]; a.fb[2] = c->tune.fullload_box[2];
   a.fb_cap = c->tune.fullload_cap;
   cudaError_t e = cudaMemsetAsync(&c->ctl->fallback_cells, 0,

@@ -191,6 +191,31 @@ __device__ __forceinline__ float4 lane_target(const float4 *__restrict__ S, int 
   return make_float4(lo(phi) + hi(phi), lo(fx) + hi(fx), lo(fy) + hi(fy), lo(fz) + hi(fz));
 }
 
+// One lane's share of one target's window: source pairs p = pb, pb + st, pb + 2 st, ... < pe
+// (st lanes share the target).  Returns (phi, sum w d) over both halves, self pair INCLUDED
+// (the caller subtracts self_phi once after combining the lanes).
+template <int KERNEL>
+__device__ __forceinline__ float4 lane_window(const float4 *__restrict__ S, float xt, float yt, float zt, int pb,
+                                              int pe, int st, const float thr, const float mc2) {
+  p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
+  p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
+  int p = pb;
+  for (; p + 3 * st < pe; p += 4 * st) {
+    const SrcPair s0 = load_pair(S, p), s1 = load_pair(S, p + st), s2 = load_pair(S, p + 2 * st),
+                  s3 = load_pair(S, p + 3 * st);
+    src_eval<KERNEL>(s0, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+    src_eval<KERNEL>(s1, xt, yt, zt, thr, mc2, phb, fxb, fyb, fzb);
+    src_eval<KERNEL>(s2, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+    src_eval<KERNEL>(s3, xt, yt, zt, thr, mc2, phb, fxb, fyb, fzb);
+  }
+  for (; p < pe; p += st) src_eval<KERNEL>(load_pair(S, p), xt, yt, zt, thr, mc2, phi, fx, fy, fz);
+  phi = add2(phi, phb);
+  fx = add2(fx, fxb);
+  fy = add2(fy, fyb);
+  fz = add2(fz, fzb);
+  return make_float4(lo(phi) + hi(phi), lo(fx) + hi(fx), lo(fy) + hi(fy), lo(fz) + hi(fz));
+}
+
 // Fallback for a target whose cell window does not fit the staging buffer: Par-Part-NoLoop
 // over global memory (Alg. 1) for target slot t in cell (cx, cy, cz).
 template <int KERNEL>

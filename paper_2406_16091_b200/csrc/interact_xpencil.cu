@@ -1,36 +1,38 @@
 // a6.3: X-pencil (Alg. 5, §5.2), re-designed for sm_100a.
 //
-// The paper's block owns an X-pencil of target cells (plus 2 ghost cells), latches one
-// target per thread in registers and then stages the <= 8 (Y, Z) +-1 neighbour pencils
-// one at a time, with a barrier before and after each (:398-407).  Here the X-pencil is a
-// whole target X-row (cy, cz) (or a segment of it) and the kernel streams rows through
-// shared memory with a producer/consumer pipeline:
+// As in the paper, the work unit is an X-pencil of target cells (a segment of L cells of one
+// X row (cy, cz), default the whole row), one thread per target ("one thread per particle",
+// :357), and the 9 pencils (cy + dy, cz + dz) around it are staged in shared memory
+// (:398-407).  B200 specifics:
 //
-//   * persistent CTAs, NC CONSUMER warps and NSLOT = 2 staging slots, each filled by its own
-//     PRODUCER warp and handed over with mbarriers (full / empty) instead of block-wide
-//     barriers: while the consumers compute a row from one slot, the other slot is staged;
-//   * staging a row (producer warp): the 9 neighbour rows' cells x0-1 .. x0+L are located in
-//     the global prefix array; each (row, cell) run of cell-sorted 16-B records (X-fastest
-//     linearisation) is copied record by record with 16-B cp.async (LDGSTS)
-//     into a MERGED layout: for every X cell the particles of its 9
-//     rows sit side by side (home row first), so the 27-cell candidate set of target cell cx
-//     is the single contiguous window [M(cx-1), M(cx+2)) -- no per-row loop, no wasted
-//     candidates.  Cell starts are padded to slot = 2j (mod 8) with inert records (x = 1e30,
-//     q = 0): windows are whole source PAIRS and the ~4 windows of a warp start in distinct
-//     bank groups.  The producer then interleaves the records in place into the source-pair
-//     layout of interact_common.cuh (bitwise copies of the fp32 inputs);
-//   * the slot capacity is fixed at launch from the mean density (the paper sizes the pencil
-//     from M_C, :353; counting actual occupancy needs no M_C read-back and no host sync): a
-//     row whose windows do not fit is split into rounds, and a cell whose window alone does
-//     not fit is handed to the consumers as a global-memory fallback item;
-//   * compute (consumer warps): one thread per target ("one thread per particle", :357), each
-//     walking its cell's window two sources per packed-fp32 instruction.
+//   * each of the 9 neighbour pencils is ONE contiguous run of cell-sorted 16-B records
+//     (X-fastest linearisation), so a pencil arrives with one TMA bulk copy
+//     (cp.async.bulk, completion counted in bytes on the slot's mbarrier): 9 copies per item,
+//     issued by a single producer warp -- no per-particle staging work at all;
+//   * persistent blocks stream the items through NSLOT = 2 slots: while the consumer warps
+//     compute one slot the producer refills the other.  Slots are handed over with mbarriers
+//     (full: TMA bytes + producer arrival; empty: one arrival per consumer warp), consumer
+//     warps take 32-target batches from a per-slot counter and move on to the next slot as
+//     soon as the current one is exhausted -- no block-wide barrier anywhere;
+//   * a target walks its 27 candidate cells as the 9 contiguous 3-cell runs (one per staged
+//     pencil); two consecutive records of a run form an f32x2 source pair
+//     (interact_common.cuh, src_eval: 12 packed-fp32 instructions + 2 MUFU.EX2 per 2
+//     candidates, differences from the raw fp32 positions);
+//   * capacity: the slot is sized from the mean density (+15 %) instead of M_C (:353), so there
+//     is no device->host read-back; a row whose 9 pencils do not fit is split into rounds
+//     along X, and a cell whose window alone does not fit takes the global-memory path.
 #include "interact_common.cuh"
 
-#ifdef XP_PROFILE
-#define XP_T(v) long long v = clock64()
-#define XP_ADD(i, a, b) if ((threadIdx.x & 31) == 0) atomicAdd(&xp_prof[i], (unsigned long long)((b) - (a)))
+#ifdef XP_PROFILE  // development counters (tools/build_prof.sh, tools/xp_prof.py)
 __device__ unsigned long long xp_prof[16];
+#define XP_T(v) long long v = clock64()
+#define XP_ADD(i, a, b) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&xp_prof[i], (unsigned long long)((b) - (a)))
+extern "C" __attribute__((visibility("default"))) void pi_debug_xp_profile(unsigned long long *out) {
+  cudaMemcpyFromSymbol(out, xp_prof, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(xp_prof, z, sizeof(z));
+}
 #else
 #define XP_T(v)
 #define XP_ADD(i, a, b)
@@ -40,390 +42,336 @@ namespace pi {
 namespace {
 
 constexpr int NSLOT = 2;
+constexpr int META = 16;
+constexpr float DUMMY_X = 1.0e30f;  // inert partner of an odd run's last record: K = 0, q = 0
 
 struct XpParams {
-  long long n;
   const float4 *rec;
+  const float4 *pairs;  // the sorted records as f32x2 source pairs (k_pairify)
   const int32_t *offsets;
   Geom g;
   KParams kp;
   OutDesc out;
   DevCtl *ctl;
   int L;             // target cells per work item along X (segment length)
-  int cap;           // staged records (incl. padding) per slot
+  int capp;          // staged source pairs per slot
   int nseg;          // segments per X row
   long long nitems;  // rows x segments
 };
 
-// Per-slot int area: meta[8] | O[9][L+3] | Dst[9][L+2] | Msz[L+2] | Moff[L+3] | Tpre[L+3]
-// meta: 0 stop flag (-1), 1 ja, 2 jb, 3 base, 4 ntargets, 5 fallback cell (or -1),
-//       6 x0, 7 (cy | cz << 16) -- written by the producer
-__host__ __device__ inline int slot_int_words(int L) {
-  int ints = 8 + 9 * (L + 3) + 9 * (L + 2) + (L + 2) + (L + 3) + (L + 3);
-  return (ints + 3) & ~3;
-}
-__host__ __device__ inline size_t slot_bytes(int L, int cap) {
-  return (size_t)slot_int_words(L) * 4 + (size_t)cap * 16;
-}
-__host__ __device__ inline size_t xp_smem_bytes(int L, int cap) {
-  return 128 /* mbarriers + reduction scratch */ + NSLOT * slot_bytes(L, cap);
-}
-
-constexpr float DUMMY_X = 1.0e30f;  // inert padding record: (x_s - x_t)^2 = inf, q = 0
+// Slot: S[2 capp] float4 (source pairs) | meta[16] | O[9][L+3] | rb[16]
+//   O[r][j]  global offsets of pencil r (= (dy + 1) + 3 (dz + 1)) at cell boundary x0-1+j
+//   rb[r]    first staged pair of pencil r's run in S (rb[9] = total)
+// meta: 0 stop (1), 1 ja, 2 jb (target cells ja..jb of the item in this round; jb < ja: the
+//       global-memory fallback for cell ja), 3 ntargets, 4 x0, 5 cy | cz << 16, 6 batch counter
+__host__ __device__ inline int slot_words(int L) { return (META + 9 * (L + 3) + 16 + 3) & ~3; }
+__host__ __device__ inline size_t slot_bytes(int L, int capp) { return (size_t)capp * 32 + (size_t)slot_words(L) * 4; }
+__host__ __device__ inline size_t xp_smem_bytes(int L, int capp) { return 128 + NSLOT * slot_bytes(L, capp); }
 
 struct Slot {
-  int *meta, *O, *Dst, *Msz, *Moff, *Tpre;
   float4 *S;
+  int *meta, *O, *rb;
 };
-__device__ __forceinline__ Slot slot_at(unsigned char *base, int L, int cap, int s) {
-  unsigned char *p = base + (size_t)s * slot_bytes(L, cap);
+__device__ __forceinline__ Slot slot_at(unsigned char *base, int L, int capp, int s) {
+  unsigned char *u = base + (size_t)s * slot_bytes(L, capp);
   Slot sl;
-  const int L3 = L + 3, L2 = L + 2;
-  sl.meta = reinterpret_cast<int *>(p);
-  sl.O = sl.meta + 8;
-  sl.Dst = sl.O + 9 * L3;
-  sl.Msz = sl.Dst + 9 * L2;
-  sl.Moff = sl.Msz + L2;
-  sl.Tpre = sl.Moff + L3;
-  sl.S = reinterpret_cast<float4 *>(p + slot_int_words(L) * 4);
+  sl.S = reinterpret_cast<float4 *>(u);
+  sl.meta = reinterpret_cast<int *>(u + (size_t)capp * 32);
+  sl.O = sl.meta + META;
+  sl.rb = sl.O + 9 * (L + 3);
   return sl;
 }
 
-// Named hardware barriers (no spinning): ids 1..NSLOT = "slot full", NSLOT+1..2 NSLOT = "slot
-// empty"; each has the producer warp of the slot and the NC consumer warps as participants.
-__device__ __forceinline__ void nbar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void nbar_arrive(int id, int nthreads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+
+// The cell-sorted records as source pairs P[2k] = (x_2k, x_2k+1, y_2k, y_2k+1),
+// P[2k+1] = (z_2k, z_2k+1, q_2k, q_2k+1) (bitwise copies; an odd count gets an inert partner),
+// so that a pencil run is staged by TMA already in the layout the f32x2 inner loop reads.
+__global__ void k_pairify(long long n, const long long *n_dev, const float4 *__restrict__ rec, float4 *P) {
+  if (n_dev) n = *n_dev;
+  const long long np = (n + 1) >> 1;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < np; k += (long long)gridDim.x * blockDim.x) {
+    const float4 a = rec[2 * k];
+    const float4 b = 2 * k + 1 < n ? rec[2 * k + 1] : make_float4(DUMMY_X, DUMMY_X, DUMMY_X, 0.f);
+    P[2 * k] = make_float4(a.x, b.x, a.y, b.y);
+    P[2 * k + 1] = make_float4(a.z, b.z, a.w, b.w);
+  }
 }
 
 // ---------------------------------------------------------------- producer (one warp)
-// Row tables of work item `item` into slot `sl`: offsets of the 9 neighbour rows, row starts
-// inside each merged cell (home row first), merged sizes, padded merged offsets.
-__device__ void build_tables(const XpParams &p, const Slot &sl, long long item, int &x0, int &cy, int &cz,
-                             int &Lseg) {
+// Offsets of the 9 pencils of `item` at the cell boundaries x0-1 .. x0+L+1 into the slot.
+__device__ void load_offsets(const XpParams &p, const Slot &sl, long long item, int &x0, int &Lseg, int &cy,
+                             int &cz) {
   const int lane = threadIdx.x & 31;
-  const int L = p.L, L3 = L + 3, L2 = L + 2;
+  const int L3 = p.L + 3;
   const Geom &g = p.g;
   const int seg = (int)(item % p.nseg);
   const long long row = item / p.nseg;
   cy = (int)(row % g.ny);
   cz = (int)(row / g.ny);
-  x0 = g.own_lo + seg * L;  // owned X cells only (ghost layers are staged as sources)
-  Lseg = min(L, g.own_hi - x0);
-  // offsets of the 9 neighbour rows over cells x0-1 .. x0+L+1: all loads issued first
-  constexpr int MAXK = (9 * 67 + 31) / 32;
-  int v[MAXK];
-#pragma unroll
-  for (int u = 0; u < MAXK; ++u) {
-    const int k = lane + 32 * u;
-    v[u] = 0;
-    if (k < 9 * L3) {
-      const int r = k / L3, j = k - r * L3;
-      const int y = cy + (r % 3) - 1, z = cz + (r / 3) - 1;
-      if (y >= 0 && y < g.ny && z >= 0 && z < g.nz) {
-        const int x = min(max(x0 - 1 + j, 0), g.nx);  // clamped: out-of-grid cells are empty
-        v[u] = __ldg(p.offsets + (long long)g.nx * (y + (long long)g.ny * z) + x);
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < MAXK; ++u) {
-    const int k = lane + 32 * u;
-    if (k < 9 * L3) sl.O[k] = v[u];
-  }
-  __syncwarp();
-  // per merged cell: row starts (home row first) and size; padded size s' = s + ((2 - s) & 7)
-  // makes every start M(j) = 2j (mod 8) with the minimal padding, and is a plain prefix sum
-  int carry = 0;
-  for (int j0 = 0; j0 < L2; j0 += 32) {
+  x0 = g.own_lo + seg * p.L;  // owned X cells only (ghost layers are staged as sources)
+  Lseg = min(p.L, g.own_hi - x0);
+  for (int j0 = 0; j0 < L3; j0 += 32) {
     const int j = j0 + lane;
-    int pre = 0;
-    if (j < L2) {
+    const int x = min(max(x0 - 1 + j, 0), g.nx);  // clamped: cells outside the grid are empty
+    int v[9];
 #pragma unroll
-      for (int rr = 0; rr < 9; ++rr) {
-        const int r = rr == 0 ? 4 : (rr <= 4 ? rr - 1 : rr);
-        sl.Dst[r * L2 + j] = pre;
-        pre += sl.O[r * L3 + j + 1] - sl.O[r * L3 + j];
-      }
-      sl.Msz[j] = pre;
+    for (int r = 0; r < 9; ++r) {
+      const int y = cy + (r % 3) - 1, z = cz + (r / 3) - 1;
+      v[r] = 0;
+      if (j < L3 && y >= 0 && y < g.ny && z >= 0 && z < g.nz)
+        v[r] = __ldg(p.offsets + (long long)g.nx * (y + (long long)g.ny * z) + x);
     }
-    const int padded = j < L2 ? pre + ((2 - pre) & 7) : 0;
-    int incl = padded;
+    if (j < L3) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
+      for (int r = 0; r < 9; ++r) sl.O[r * L3 + j] = v[r];
     }
-    if (j < L2) sl.Moff[j] = carry + incl - padded;
-    carry += __shfl_sync(0xffffffffu, incl, 31);
   }
-  if (lane == 0) sl.Moff[L2] = carry;
   __syncwarp();
 }
 
-// Chooses the round [ja, jb] (warp-cooperative), issues its TMA copies, writes padding and
-// the slot meta.  jb < ja means "cell ja needs the fallback".
-__device__ int stage_round(const XpParams &p, const Slot &sl, unsigned long long *tma_bar, int ja, int Lseg) {
+// Round [ja, jb] of the item: the largest jb <= Lseg whose 9 pencil runs (cells ja-1 .. jb+1,
+// whole source pairs) fit the slot (warp-uniform; jb < ja: cell ja alone does not fit).
+__device__ int choose_round(const XpParams &p, const Slot &sl, int ja, int Lseg) {
   const int lane = threadIdx.x & 31;
-  const int L = p.L, L3 = L + 3, L2 = L + 2;
-  const int base = sl.Moff[ja - 1];
+  const int L3 = p.L + 3;
   int jb = ja - 1;
   for (int j0 = ja; j0 <= Lseg; j0 += 32) {
     const int j = j0 + lane;
-    const bool fit = j <= Lseg && sl.Moff[j + 2] - base <= p.cap;
-    const unsigned b = __ballot_sync(0xffffffffu, fit);
+    int tot = 0;
+    if (j <= Lseg) {
+#pragma unroll
+      for (int r = 0; r < 9; ++r) tot += ((sl.O[r * L3 + j + 2] + 1) >> 1) - (sl.O[r * L3 + ja - 1] >> 1);
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, j <= Lseg && tot <= p.capp);
     jb += __popc(b);
     if (b != 0xffffffffu) break;
-  }
-  if (jb < ja) return jb;
-  // target prefix over the round's cells
-  int carry = 0;
-  for (int j0 = ja; j0 <= jb; j0 += 32) {
-    const int j = j0 + lane;
-    const int nt = j <= jb ? sl.O[4 * L3 + j + 1] - sl.O[4 * L3 + j] : 0;
-    int incl = nt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (j <= jb) sl.Tpre[j] = carry + incl - nt;
-    carry += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  if (lane == 0) sl.Tpre[jb + 1] = carry;
-  int real = 0;
-  for (int j = ja - 1 + lane; j <= jb + 1; j += 32) real += sl.Msz[j];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) real += __shfl_xor_sync(0xffffffffu, real, o);
-  (void)real;
-  (void)tma_bar;
-  // one (row, cell) run per lane, each record one 16-B cp.async (LDGSTS) into its merged slot
-  const int ncell = jb - ja + 3;
-  for (int k = lane; k < 9 * ncell; k += 32) {
-    const int jj = k / 9, r = k - jj * 9;
-    const int j = ja - 1 + jj;
-    const int src = sl.O[r * L3 + j];
-    const int c = sl.O[r * L3 + j + 1] - src;
-    float4 *dst = sl.S + (sl.Moff[j] + sl.Dst[r * L2 + j] - base);
-    const float4 *gs = p.rec + src;
-    for (int e = 0; e < c; ++e) cp_async16(dst + e, gs + e);
-  }
-  // padding records (disjoint from the bulk-copy destinations)
-  for (int k = lane; k < 8 * ncell; k += 32) {
-    const int jj = k >> 3, u = k & 7;
-    const int j = ja - 1 + jj;
-    const int s = sl.Moff[j] + sl.Msz[j] + u;
-    if (s < sl.Moff[j + 1]) sl.S[s - base] = make_float4(DUMMY_X, DUMMY_X, DUMMY_X, 0.f);
-  }
-  if (lane == 0) {
-    sl.meta[1] = ja;
-    sl.meta[2] = jb;
-    sl.meta[3] = base;
-    sl.meta[4] = carry;
-    sl.meta[5] = -1;
   }
   return jb;
 }
 
-template <int KERNEL, int NC, int UNR>
-__global__ void __launch_bounds__((NC + NSLOT) * 32, 2) k_interact_xpencil(XpParams p) {
+// ---------------------------------------------------------------- consumer
+// (phi, sum w d) of the target `me` over the 9 runs of cell j (cells j-1 .. j+1 of every
+// pencil).  A run [a, b) of records covers the staged pairs a/2 .. (b-1)/2; the halves of its
+// first and last pair that lie outside the run get q = 0 (they add exactly 0).  The self
+// term (= q_t exactly: d = 0, K(0) = 2^0 = 1) is removed.
+template <int KERNEL>
+__device__ __forceinline__ float4 walk9(const Slot &sl, int L3, int ja, int j, const float4 me, const float thr,
+                                        const float mc2) {
+  const float4 *__restrict__ S = sl.S;
+  p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
+  p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
+#pragma unroll 1
+  for (int r = 0; r < 9; ++r) {
+    const int a = sl.O[r * L3 + j - 1], b = sl.O[r * L3 + j + 2];
+    if (b <= a) continue;
+    const int base = sl.rb[r] - (sl.O[r * L3 + ja - 1] >> 1);
+    const int p0 = base + (a >> 1), pl = base + ((b - 1) >> 1);  // first and last pair
+    {
+      SrcPair f = load_pair(S, p0);
+      f.q = pk((a & 1) ? 0.f : lo(f.q), (p0 == pl && (b & 1)) ? 0.f : hi(f.q));
+      src_eval<KERNEL>(f, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz);
+    }
+    if (pl > p0) {
+      int q = p0 + 1;
+      for (; q + 2 <= pl; q += 2) {
+        const SrcPair s0 = load_pair(S, q), s1 = load_pair(S, q + 1);
+        src_eval<KERNEL>(s0, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb);
+        src_eval<KERNEL>(s1, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz);
+      }
+      if (q < pl) src_eval<KERNEL>(load_pair(S, q), me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb);
+      SrcPair l = load_pair(S, pl);
+      l.q = pk(lo(l.q), (b & 1) ? 0.f : hi(l.q));
+      src_eval<KERNEL>(l, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb);
+    }
+  }
+  phi = add2(phi, phb);
+  fx = add2(fx, fxb);
+  fy = add2(fy, fyb);
+  fz = add2(fz, fzb);
+  // identity exclusion (Alg. 1 :127): the self pair added exactly q_t to phi and 0 to F
+  return make_float4(lo(phi) + hi(phi) - me.w, lo(fx) + hi(fx), lo(fy) + hi(fy), lo(fz) + hi(fz));
+}
+
+template <int KERNEL, int NC>
+__global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem_raw);  // [NSLOT]
   unsigned long long *empty = full + NSLOT;                                      // [NSLOT]
-  unsigned long long *tmab = empty + NSLOT;                                      // [NSLOT]
-  unsigned long long *red = reinterpret_cast<unsigned long long *>(smem_raw + 64);  // [8]
   unsigned char *slots = smem_raw + 128;
   const int L = p.L, L3 = L + 3;
   const Geom &g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned long long cand = 0, fallbacks = 0;
 
-  (void)full;
-  (void)empty;
-  (void)tmab;
-  constexpr int NPART = (NC + 1) * 32;  // participants of a slot barrier
-  if (tid < 8) red[tid] = 0;
+  if (tid == 0) {
+    for (int k = 0; k < NSLOT; ++k) {
+      mbar_init(&full[k], 1);    // producer lane 0 (arrive.expect_tx) + the TMA bytes
+      mbar_init(&empty[k], NC);  // one arrival per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
 
-  if (warp >= NC) {
-    // ============================ producers (one per slot) ============================
-    unsigned used = 0;
-    const int slot = warp - NC;
-    bool done = false;
-    while (!done) {
-      long long item = 0;
-      if (lane == 0) item = (long long)atomicAdd(&p.ctl->xp_items, 1ull);
-      item = __shfl_sync(0xffffffffu, item, 0);
-      int x0 = 0, cy = 0, cz = 0, Lseg = 0;
-      int ja = 1;
-      bool first = true;
-      while (first || ja <= Lseg) {
-        Slot sl = slot_at(slots, L, p.cap, slot);
-        if (used & (1u << slot)) {  // wait until the consumers released this slot
-          XP_T(t0);
-          nbar_sync(1 + NSLOT + slot, NPART);
-          XP_T(t1);
-          XP_ADD(0, t0, t1);
-        }
-        used |= 1u << slot;
-        if (item >= p.nitems) {  // stop marker
-          if (lane == 0) sl.meta[0] = -1;
-          __syncwarp();
-          nbar_arrive(1 + slot, NPART);
-          done = true;
+  if (warp == NC) {
+    // ================================ producer ================================
+    long long item = -1;
+    int x0 = 0, Lseg = 0, cy = 0, cz = 0, ja = 1;
+    for (unsigned use = 0;; ++use) {
+      const int s = use % NSLOT;
+      const Slot sl = slot_at(slots, L, p.capp, s);
+      XP_T(t0);
+      if (use >= NSLOT) mbar_wait(&empty[s], ((use / NSLOT) - 1) & 1);  // consumers released it
+      XP_T(t1);
+      XP_ADD(0, t0, t1);
+      fence_proxy_async();  // their generic reads of the slot precede the TMA writes below
+      if (item < 0 || ja > Lseg) {
+        if (lane == 0) item = (long long)atomicAdd(&p.ctl->xp_items, 1ull);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= p.nitems) {  // stop marker: consumers leave at the first one
+          if (lane == 0) {
+            sl.meta[0] = 1;
+            mbar_arrive(&full[s]);
+          }
           break;
         }
-        XP_T(t2);
-        build_tables(p, sl, item, x0, cy, cz, Lseg);
-        XP_T(t3);
-        XP_ADD(1, t2, t3);
-        first = false;
-        const int jb = stage_round(p, sl, &tmab[slot], ja, Lseg);
-        XP_T(t4);
-        XP_ADD(2, t3, t4);
-        if (lane == 0) {
-          sl.meta[0] = 0;
-          sl.meta[6] = x0;
-          sl.meta[7] = cy | (cz << 16);
-        }
-        if (jb < ja) {  // fallback cell: consumers run the global path for cell ja
-          if (lane == 0) {
-            sl.meta[1] = ja;
-            sl.meta[2] = ja - 1;
-            sl.meta[4] = 0;
-            sl.meta[5] = ja;
-          }
-          ++ja;
-        } else {
-          cp_async_wait_all();
-          XP_T(t5);
-          XP_ADD(3, t4, t5);
-          __syncwarp();
-          // interleave in place: raw record pairs -> source-pair layout
-          const int total = sl.Moff[jb + 2] - sl.Moff[ja - 1];
-          int k = lane;
-          for (; k + 96 < (total >> 1); k += 128) {
-            stage_pair(sl.S, k);
-            stage_pair(sl.S, k + 32);
-            stage_pair(sl.S, k + 64);
-            stage_pair(sl.S, k + 96);
-          }
-          for (; k < (total >> 1); k += 32) stage_pair(sl.S, k);
-          ja = jb + 1;
-        }
+        load_offsets(p, sl, item, x0, Lseg, cy, cz);
+        ja = 1;
+      } else {
+        // next round of the same item: the offsets are reused (copy them into this slot)
+        const Slot prev = slot_at(slots, L, p.capp, (use - 1) % NSLOT);
+        for (int k = lane; k < 9 * L3; k += 32) sl.O[k] = prev.O[k];
         __syncwarp();
-        XP_T(t6);
-        XP_ADD(4, t4, t6);
-        XP_ADD(5, t2, t6);
-        nbar_arrive(1 + slot, NPART);  // release: tables, records, meta
       }
+      const int jb = choose_round(p, sl, ja, Lseg);
+      // run of pencil r: cells ja-1 .. jb+1 (just cell ja's window for a fallback round)
+      const int last = jb < ja ? ja : jb;
+      int a = 0, len = 0;  // pairs of pencil run `lane`
+      if (lane < 9) {
+        a = sl.O[lane * L3 + ja - 1] >> 1;
+        len = jb < ja ? 0 : ((sl.O[lane * L3 + last + 2] + 1) >> 1) - a;
+      }
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 8);
+      if (lane < 9) sl.rb[lane] = incl - len;
+      if (lane == 0) {
+        sl.rb[9] = total;
+        sl.meta[0] = 0;
+        sl.meta[1] = ja;
+        sl.meta[2] = jb;
+        sl.meta[3] = sl.O[4 * L3 + last + 1] - sl.O[4 * L3 + ja];
+        sl.meta[4] = x0;
+        sl.meta[5] = cy | (cz << 16);
+        sl.meta[6] = 0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], (unsigned)total * 32u);  // release: tables
+      __syncwarp();
+      if (lane < 9 && len > 0) bulk_g2s(sl.S + 2 * (incl - len), p.pairs + 2 * (long long)a, (unsigned)len * 32u, &full[s]);
+      ja = last + 1;
+      XP_T(t2);
+      XP_ADD(1, t1, t2);
+      XP_ADD(2, 0, 1);
     }
   } else {
     // ================================ consumers ================================
     const float thr = p.kp.rc2, mc2 = -p.kp.c2;
-    unsigned stopped = 0;  // one bit per slot
-    int slot = 0;
-    while (stopped != (1u << NSLOT) - 1u) {
-      if (stopped & (1u << slot)) {
-        slot = (slot + 1) % NSLOT;
-        continue;
-      }
+    for (unsigned use = 0;; ++use) {
+      const int s = use % NSLOT;
+      const Slot sl = slot_at(slots, L, p.capp, s);
       XP_T(c0);
-      nbar_sync(1 + slot, NPART);
+      mbar_wait(&full[s], (use / NSLOT) & 1);
       XP_T(c1);
-      XP_ADD(6, c0, c1);
-      Slot sl = slot_at(slots, L, p.cap, slot);
-      if (sl.meta[0] < 0) {  // this slot's producer ran out of work items
-        stopped |= 1u << slot;
-        slot = (slot + 1) % NSLOT;
-        continue;
-      }
-      const int ja = sl.meta[1], jb = sl.meta[2], base = sl.meta[3], ntargets = sl.meta[4], fb = sl.meta[5];
-      const int x0 = sl.meta[6], cy = sl.meta[7] & 0xffff, cz = sl.meta[7] >> 16;
-      if (fb >= 0) {
-        // global-memory fallback for one cell, spread over the consumer threads
-        const long long home_row = (long long)g.nx * (cy + (long long)g.ny * cz);
-        const int cx = x0 - 1 + fb;
-        const int t_lo = __ldg(p.offsets + home_row + cx), t_hi = __ldg(p.offsets + home_row + cx + 1);
-        for (int t = t_lo + tid; t < t_hi; t += NC * 32)
-          fallback_target<KERNEL>(t, cx, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand);
-        if (tid == 0) ++fallbacks;
-      } else {
-        for (int T = tid; T < ntargets; T += NC * 32) {
-          // cell of target T: last j in [ja, jb] with Tpre[j] <= T (binary search)
-          int lo_ = ja, hi_ = jb;
-          while (lo_ < hi_) {
-            const int mid = (lo_ + hi_ + 1) >> 1;
-            if (sl.Tpre[mid] <= T) lo_ = mid; else hi_ = mid - 1;
-          }
-          const int j = lo_;
-          const int i = T - sl.Tpre[j];
-          const int t = sl.Moff[j] - base + i;  // staged slot of the target
-          const int p0 = (sl.Moff[j - 1] - base) >> 1, p1 = (sl.Moff[j + 2] - base) >> 1;
-          const float4 r = lane_target<KERNEL, UNR>(sl.S, t >> 1, t & 1, p0, p1, thr, mc2);
-          cand += (unsigned long long)(sl.Msz[j - 1] + sl.Msz[j] + sl.Msz[j + 1] - 1);
-          const int gs = sl.O[4 * L3 + j] + i;
-          float4 me = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (p.out.upd) me = __ldg(p.rec + gs);
-          if (KERNEL == PI_K_GAUSSIAN) {
-            const float4 qq = sl.S[2 * (t >> 1) + 1];
-            const float q = (t & 1) ? qq.w : qq.z;
-            const float sc = -q * p.kp.inv_s2;
-            write_output(p.out, g, gs, me, r.x, sc * r.y, sc * r.z, sc * r.w);
+      XP_ADD(3, c0, c1);
+      if (sl.meta[0]) break;  // out of work items
+      const int ja = sl.meta[1], jb = sl.meta[2], ntargets = sl.meta[3], x0 = sl.meta[4];
+      const int cy = sl.meta[5] & 0xffff, cz = sl.meta[5] >> 16;
+      const int *O4 = sl.O + 4 * L3;
+      const int t0 = O4[ja];  // global sorted index of the round's first target
+      for (;;) {
+        int b = 0;
+        if (lane == 0) b = atomicAdd(&sl.meta[6], 32);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b >= ntargets) break;
+        const int T = b + lane;
+        if (T < ntargets) {
+          const int gs = t0 + T;
+          if (jb < ja) {  // fallback round: cell ja from global memory
+            fallback_target<KERNEL>(gs, x0 - 1 + ja, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand);
+            if (T == 0) ++fallbacks;
           } else {
-            write_output(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f);
+            // cell of the target: last j in [ja, jb] with O4[j] <= gs
+            int lo_ = ja, hi_ = jb;
+            while (lo_ < hi_) {
+              const int mid = (lo_ + hi_ + 1) >> 1;
+              if (O4[mid] <= gs) lo_ = mid; else hi_ = mid - 1;
+            }
+            const int j = lo_;
+            const int tp = sl.rb[4] - (sl.O[4 * L3 + ja - 1] >> 1) + (gs >> 1);  // the target's pair
+            const float4 ua = sl.S[2 * tp], ub = sl.S[2 * tp + 1];
+            const float4 me = (gs & 1) ? make_float4(ua.y, ua.w, ub.y, ub.w) : make_float4(ua.x, ua.z, ub.x, ub.z);
+            const float4 r = walk9<KERNEL>(sl, L3, ja, j, me, thr, mc2);
+            int nc = 0;
+#pragma unroll
+            for (int rr = 0; rr < 9; ++rr) nc += sl.O[rr * L3 + j + 2] - sl.O[rr * L3 + j - 1];
+            cand += (unsigned long long)(nc - 1);
+            if (KERNEL == PI_K_GAUSSIAN) {
+              const float sc = -me.w * p.kp.inv_s2;
+              write_output(p.out, g, gs, me, r.x, sc * r.y, sc * r.z, sc * r.w);
+            } else {
+              write_output(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f);
+            }
           }
         }
       }
       __syncwarp();
       XP_T(c2);
-      XP_ADD(7, c1, c2);
-      XP_ADD(8, 0, 1);
-      nbar_arrive(1 + NSLOT + slot, NPART);
-      slot = (slot + 1) % NSLOT;
+      XP_ADD(4, c1, c2);
+      XP_ADD(5, 0, 1);
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
   }
-  // statistics: one atomic per block, spread over CAND_SLOTS counters
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cand += __shfl_xor_sync(0xffffffffu, cand, o);
-  if (lane == 0 && cand) atomicAdd(&red[warp & 7], cand);
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long tsum = 0;
-    for (int w = 0; w < 8; ++w) tsum += red[w];
-    if (tsum) atomicAdd(&p.ctl->cand_slots[blockIdx.x & (CAND_SLOTS - 1)], tsum);
-  }
-  if (tid < NC * 32 && (tid & 31) == 0 && fallbacks) atomicAdd(&p.ctl->fallback_cells, fallbacks);
-}
 
-template <int KERNEL, int NC>
-cudaError_t launch_k(const XpParams &p, cudaStream_t s, int blocks_per_sm) {
-  constexpr int UNR = NC >= 16 ? 2 : 4;  // registers: 2 blocks x (NC + 2) warps must fit
-  const size_t smem = xp_smem_bytes(p.L, p.cap);
-  cudaError_t e =
-      cudaFuncSetAttribute(k_interact_xpencil<KERNEL, NC, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_interact_xpencil<KERNEL, NC, UNR>, (NC + NSLOT) * 32, smem);
-  if (occ < 1) occ = 1;
-  long long blocks = (long long)sms * (blocks_per_sm > 0 ? min(occ, blocks_per_sm) : occ);
-  if (blocks > p.nitems) blocks = p.nitems;
-  if (blocks < 1) blocks = 1;
-  k_interact_xpencil<KERNEL, NC, UNR><<<(int)blocks, (NC + NSLOT) * 32, smem, s>>>(p);
-  return cudaGetLastError();
+  // statistics: warp-level sums, spread over CAND_SLOTS counters
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cand += __shfl_xor_sync(0xffffffffu, cand, o);
+    fallbacks += __shfl_xor_sync(0xffffffffu, fallbacks, o);
+  }
+  if (lane == 0) {
+    if (cand) atomicAdd(&p.ctl->cand_slots[(blockIdx.x * (NC + 1) + warp) & (CAND_SLOTS - 1)], cand);
+    if (fallbacks) atomicAdd(&p.ctl->fallback_cells, fallbacks);
+  }
 }
 
 template <int NC>
-cudaError_t launch_nc(const XpParams &p, cudaStream_t s, int bps) {
+cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
+  const size_t smem = xp_smem_bytes(p.L, p.capp);
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (NC + 1) * 32, smem);
+    if (occ < 1) occ = 1;
+    long long blocks = (long long)sms * occ;
+    if (blocks > p.nitems) blocks = p.nitems;
+    if (blocks < 1) blocks = 1;
+    kern<<<(int)blocks, (NC + 1) * 32, smem, s>>>(p);
+    return cudaGetLastError();
+  };
   switch (p.kp.kernel) {
-    case PI_K_GAUSSIAN: return launch_k<PI_K_GAUSSIAN, NC>(p, s, bps);
-    case PI_K_INDICATOR: return launch_k<PI_K_INDICATOR, NC>(p, s, bps);
-    default: return launch_k<PI_K_CANDIDATE, NC>(p, s, bps);
+    case PI_K_GAUSSIAN: return go(k_interact_xpencil<PI_K_GAUSSIAN, NC>);
+    case PI_K_INDICATOR: return go(k_interact_xpencil<PI_K_INDICATOR, NC>);
+    default: return go(k_interact_xpencil<PI_K_CANDIDATE, NC>);
   }
 }
 
@@ -432,7 +380,6 @@ cudaError_t launch_nc(const XpParams &p, cudaStream_t s, int bps) {
 cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s) {
   if (a.n <= 0) return cudaSuccess;
   XpParams p;
-  p.n = a.n;
   p.rec = a.rec;
   p.offsets = a.offsets;
   p.g = g;
@@ -440,35 +387,35 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   p.out = a.out;
   p.ctl = a.ctl;
   const int own = g.own_hi - g.own_lo;
-  p.L = a.tx_len > 0 ? a.tx_len : 32;
-  if (p.L > 64) p.L = 64;
+  p.L = a.tx_len > 0 ? a.tx_len : 64;
+  if (p.L > 128) p.L = 128;
   if (p.L > own) p.L = own;
   p.nseg = (own + p.L - 1) / p.L;
   p.nitems = (long long)p.nseg * g.ny * g.nz;
-  // consumer warps (threads = 32 * NC target threads + one producer warp)
-  const int nc = a.threads == 512 ? 16 : (a.threads == 128 ? 4 : 8);
-  if (a.tx_cap > 0) {
-    p.cap = a.tx_cap;
-  } else {
-    // mean occupancy of 9 rows x (L + 2) cells (+ 10 %), plus the padding (< 8 per cell)
+  const int nc = a.threads > 0 ? a.threads / 32 : 20;
+  int cap = a.tx_cap;
+  if (cap <= 0) {
+    // mean occupancy of 9 pencils x (L + 2) cells + 15 %, plus a few records
     const double ppc = (double)a.n_est / (double)g.ncells;
-    p.cap = (int)((9.0 * ppc * 1.1 + 4.0) * (p.L + 2) + 128.0);
+    cap = (int)(9.0 * ppc * 1.15 * (p.L + 2) + 64.0);
   }
-  p.cap = (p.cap + 31) & ~31;
+  p.capp = max(16, cap / 2 + 9);  // + one partial pair per run
   const size_t max_smem = 227 * 1024;
-  while (xp_smem_bytes(p.L, p.cap) > max_smem && p.cap > 64) p.cap -= 32;
-  const int bps = a.groups;  // blocks-per-SM cap (tuning knob lanes_per_pair reused), 0 = occupancy
-  if (nc == 4) return launch_nc<4>(p, s, bps);
-  if (nc == 8) return launch_nc<8>(p, s, bps);
-  return launch_nc<16>(p, s, bps);
+  while (xp_smem_bytes(p.L, p.capp) > max_smem && p.capp > 64) p.capp -= 32;
+  if (xp_smem_bytes(p.L, p.capp) > max_smem) return cudaErrorNotSupported;
+  p.pairs = a.pairs;
+  {
+    const long long np = (a.n + 1) / 2;
+    int blocks = (int)min((np + 255) / 256, 148LL * 16);
+    k_pairify<<<max(blocks, 1), 256, 0, s>>>(a.n, a.n_dev, a.rec, a.pairs);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (nc <= 4) return launch_nc<4>(p, s);
+  if (nc <= 8) return launch_nc<8>(p, s);
+  if (nc <= 16) return launch_nc<16>(p, s);
+  if (nc <= 20) return launch_nc<20>(p, s);
+  return launch_nc<24>(p, s);
 }
 
 }  // namespace pi
-
-#ifdef XP_PROFILE
-extern "C" __attribute__((visibility("default"))) void pi_debug_xp_profile(unsigned long long *out) {
-  cudaMemcpyFromSymbol(out, xp_prof, sizeof(unsigned long long) * 16);
-  unsigned long long z[16] = {0};
-  cudaMemcpyToSymbol(xp_prof, z, sizeof(z));
-}
-#endif

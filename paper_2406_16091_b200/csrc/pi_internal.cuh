@@ -169,6 +169,7 @@ struct InteractArgs {
   const long long *n_dev;       // device-resident count (nranks > 1), or NULL
   long long n_est;              // host estimate of the sorted count (sizes staging buffers)
   const float4 *rec;            // sorted records
+  float4 *pairs;                // scratch [2 * (n / 2 + 1)]: the records as f32x2 source pairs
   const int32_t *offsets;       // [ncells + 1]
   OutDesc out;
   DevCtl *ctl;

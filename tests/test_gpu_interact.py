@@ -142,10 +142,13 @@ def test_xpencil_tuning_shapes(algo):
     c = synth.scaled_uniform(8, (20, 6, 5), seed=3)
     want = oracle_interact(c)
     for tune in (dict(xpencil_len=1), dict(xpencil_len=7, xpencil_cap=300), dict(xpencil_len=64),
-                 dict(xpencil_len=16, xpencil_cap=64), dict(threads=256, xpencil_len=5),
-                 dict(lanes_per_pair=1), dict(lanes_per_pair=4, threads=256), dict(lanes_per_pair=4)):
-        got, _ = gpu_interact(c, algo, tuning=tune)
+                 dict(xpencil_len=16, xpencil_cap=64), dict(threads=256, xpencil_len=5), dict(threads=32),
+                 dict(xpencil_cap=16), dict(lanes_per_target=1), dict(lanes_per_target=3),
+                 dict(lanes_per_target=4, threads=256), dict(lanes_per_target=4)):
+        got, ctx = gpu_interact(c, algo, tuning=tune)
         assert_parity(got, want, label=f"{algo} {tune}")
+        if algo == "xpencil" and tune.get("xpencil_cap") in (16, 64):
+            assert ctx.stats()["fallback_cells"] > 0  # merged cells over the cap take the global path
 
 
 def test_fullload_tuning_shapes():

@@ -10,15 +10,22 @@ t = [torch.from_numpy(v).cuda() for v in (c.x, c.y, c.z, c.q)]
 ctx.bin(*t)
 lib = L.load()
 buf = (ctypes.c_ulonglong * 16)()
-for tune in ({}, {"xpencil_len": 64}, {"threads": 512}):
+mode = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+# (no modes)
+for tune in ({}, {"xpencil_len": 32}):
     ctx.set_tuning(**tune)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ctx.interact("xpencil", out=False)
+    e1.record(); torch.cuda.synchronize()
+    print("mode", mode, tune, "kernel ms", e0.elapsed_time(e1))
     ctx.interact("xpencil", out=False); torch.cuda.synchronize()
     lib.pi_debug_xp_profile(buf)
     ctx.interact("xpencil", out=False); torch.cuda.synchronize()
     lib.pi_debug_xp_profile(buf)
     v = list(buf)
-    items = 8192 if not tune.get("xpencil_len") else 4096
-    names = ["prod wait empty", "prod tables", "prod stage_round", "prod cp.async wait", "prod stage->arrive", "prod total", "cons wait full", "cons compute", "cons warp-items"]
+    items = 4096 * 64 // tune.get("xpencil_len", 64)
+    names = ["prod wait empty", "prod fill", "prod uses", "cons wait full", "cons compute", "cons warp-uses"]
     print(tune)
     for i, n in enumerate(names):
         print(f"  {n:22s} {v[i]:16d}  per item {v[i]/items:12.0f}")
