@@ -14,6 +14,12 @@
 //   k_scatter a4: "move the particles in a secondary array (not in-place)" (:64): slot =
 //             offsets[cell] + rank; writes one 16-byte (x, y, z, q) record per particle
 //             (a full 16-B store instead of four 4-B scattered stores) plus its id.
+//   AoS path  (pi_step re-binning of the nearly sorted updated state): the count pass only
+//             counts (no rank array: 16 B read per particle), the scan keeps the counts, and the
+//             scatter takes each rank with an atomicSub on them, which leaves the counts zero
+//             for the next binning -- 8 B per particle less traffic than storing ranks.  Both
+//             aggregate over runs of equal cells among consecutive lanes (shuffle + ballot),
+//             one atomic per run, since that input is nearly sorted.
 #include "pi_internal.cuh"
 
 namespace pi {
@@ -91,22 +97,54 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_count_soa(long long n, const 
   if (bad) atomicOr(&ctl->flags, FLAG_OUT_OF_BOX);
 }
 
-// a1 + a2 over AoS records (pi_step re-binning of the updated sorted state).
+// Runs of equal cells among consecutive lanes (the nearly sorted AoS input): one atomic per
+// run.  Returns the run's first lane and length for this lane (invalid lanes: runs of one).
+__device__ __forceinline__ void lane_run(int lin, bool valid, int &head, int &len) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int key = valid ? lin : -1 - lane;
+  const int prev = __shfl_up_sync(full, key, 1);
+  const unsigned heads = __ballot_sync(full, lane == 0 || prev != key);
+  head = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));  // last head at or below this lane
+  const unsigned above = heads & ~(0xffffffffu >> (31 - lane));  // heads above this lane
+  const int next = above ? __ffs(above) - 1 : 32;
+  len = next - head;
+}
+
+// Count pass of the AoS path: one atomicAdd per run of equal cells.
+__device__ __forceinline__ void run_count(int32_t *counts, int lin, bool valid) {
+  int head, len;
+  lane_run(lin, valid, head, len);
+  if (valid && (int)(threadIdx.x & 31) == head) atomicAdd(counts + lin, len);
+}
+
+// Scatter of the AoS path: a distinct rank in [0, count) per particle, taken from the counts
+// with one atomicSub per run (which leaves the counts zero).
+__device__ __forceinline__ int run_take(int32_t *counts, int lin, bool valid) {
+  int head, len;
+  lane_run(lin, valid, head, len);
+  const int lane = threadIdx.x & 31;
+  int top = 0;
+  if (valid && lane == head) top = atomicSub(counts + lin, len);
+  top = __shfl_sync(0xffffffffu, top, head);
+  return top - len + (lane - head);
+}
+
+// a1 + a2 over AoS records (pi_step re-binning of the updated sorted state): counts only,
+// one atomic per run of equal cells in a warp.
 __global__ void __launch_bounds__(COUNT_THREADS) k_count_aos(long long n, const float4 *__restrict__ rec, Geom g,
-                                                              int32_t *__restrict__ counts,
-                                                              int32_t *__restrict__ rank, DevCtl *ctl,
+                                                              int32_t *__restrict__ counts, DevCtl *ctl,
                                                               const long long *n_dev) {
   if (n_dev) n = *n_dev;
   bool bad = false;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    bool ok = i < n;
-    float4 r = ok ? __ldg(rec + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
+    const long long i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    const float4 r = ok ? __ldg(rec + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     bool b = false;
-    int lin = cell_lin(g, r.x, r.y, r.z, b);
+    const int lin = cell_lin(g, r.x, r.y, r.z, b);
     bad |= ok && b;
-    int rk = agg_increment(counts, lin, ok);
-    if (ok) rank[i] = rk;
+    run_count(counts, lin, ok);
   }
   if (bad) atomicOr(&ctl->flags, FLAG_OUT_OF_BOX);
 }
@@ -126,6 +164,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
   return v;
 }
 
+template <bool KEEP>  // KEEP: leave the counts (the scatter consumes them)
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t *__restrict__ counts,
                                                        int32_t *__restrict__ offsets,
                                                        unsigned long long *__restrict__ status, int num_tiles,
@@ -151,14 +190,14 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
     for (int k = 0; k < SCAN_ITEMS / 4; ++k) {
       int4 a = p[k];
       v[4 * k] = a.x; v[4 * k + 1] = a.y; v[4 * k + 2] = a.z; v[4 * k + 3] = a.w;
-      p[k] = make_int4(0, 0, 0, 0);  // leave zeroed counts for the next binning
+      if (!KEEP) p[k] = make_int4(0, 0, 0, 0);  // leave zeroed counts for the next binning
     }
   } else {
 #pragma unroll
     for (int k = 0; k < SCAN_ITEMS; ++k) {
       long long c = base + k;
       v[k] = c < ncells ? counts[c] : 0;
-      if (c < ncells) counts[c] = 0;
+      if (!KEEP && c < ncells) counts[c] = 0;
     }
   }
   int mx = 0, sum = 0;
@@ -253,8 +292,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
   }
 }
 
-// a4: out-of-place scatter.  SoA input (pi_bin) or AoS records (pi_step).
-template <bool AOS>
+// a4: out-of-place scatter.  SoA input (pi_bin) or AoS records (pi_step); TAKE: ranks from
+// the counts (counted mode) instead of the count pass.
+template <bool AOS, bool TAKE = false>
 __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const float *__restrict__ x,
                                                             const float *__restrict__ y,
                                                             const float *__restrict__ z,
@@ -269,17 +309,28 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
                                                             const int32_t *__restrict__ perm_in,
                                                             const long long *n_dev) {
   if (n_dev) n = *n_dev;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    float4 r;
-    if (AOS) {
-      r = __ldg(rec_in + i);
-    } else {
-      r = make_float4(__ldg(x + i), __ldg(y + i), __ldg(z + i), __ldg(q + i));
+  for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
+    const long long i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    if (!TAKE && !ok) break;
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ok) {
+      if (AOS) {
+        r = __ldg(rec_in + i);
+      } else {
+        r = make_float4(__ldg(x + i), __ldg(y + i), __ldg(z + i), __ldg(q + i));
+      }
     }
     bool b = false;
     int lin = cell_lin(g, r.x, r.y, r.z, b);
-    int slot = __ldg(offsets + lin) + __ldg(rank + i);
+    int rk;
+    if (TAKE) {
+      rk = run_take(const_cast<int32_t *>(rank), lin, ok);  // rank = the counts array here
+      if (!ok) continue;
+    } else {
+      rk = __ldg(rank + i);
+    }
+    int slot = __ldg(offsets + lin) + rk;
     rec_out[slot] = r;
     sid_out[slot] = id_in ? __ldg(id_in + i) : (int32_t)i;
     if (perm_out) perm_out[slot] = perm_in ? __ldg(perm_in + i) : (int32_t)i;
@@ -299,28 +350,26 @@ int grid_for(long long work, int threads) {
 int scan_tiles(long long ncells) { return (int)((ncells + SCAN_TILE - 1) / SCAN_TILE); }
 
 cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
-  if (a.n > 0) {
-    if (a.rec_in) {
-      k_count_aos<<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.rec_in, g, a.counts, a.rank,
-                                                                         a.ctl, a.n_dev);
-    } else {
-      k_count_soa<<<grid_for((a.n + 3) / 4, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.x, a.y, a.z, g,
-                                                                                   a.counts, a.rank, a.cell_of,
-                                                                                   a.ctl);
-    }
-  }
-  int tiles = scan_tiles(g.ncells);
-  k_scan<<<tiles, SCAN_THREADS, 0, s>>>(g.ncells, a.counts, a.offsets, a.tile_status, tiles, a.ctl);
-  if (a.n > 0) {
-    if (a.rec_in)
-      k_scatter<true><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
-          a.n, nullptr, nullptr, nullptr, nullptr, a.rec_in, a.id_in, g, a.rank, a.offsets, a.rec_out, a.sid_out,
+  const int tiles = scan_tiles(g.ncells);
+  if (a.rec_in) {  // AoS: count, scan keeping the counts, scatter taking ranks from them
+    if (a.n > 0)
+      k_count_aos<<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.rec_in, g, a.counts, a.ctl, a.n_dev);
+    k_scan<true><<<tiles, SCAN_THREADS, 0, s>>>(g.ncells, a.counts, a.offsets, a.tile_status, tiles, a.ctl);
+    if (a.n > 0)
+      k_scatter<true, true><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
+          a.n, nullptr, nullptr, nullptr, nullptr, a.rec_in, a.id_in, g, a.counts, a.offsets, a.rec_out, a.sid_out,
           a.perm_out, a.perm_in, a.n_dev);
-    else
-      k_scatter<false><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
-          a.n, a.x, a.y, a.z, a.q, nullptr, a.id_in, g, a.rank, a.offsets, a.rec_out, a.sid_out, a.perm_out, nullptr,
-          nullptr);
+    return cudaGetLastError();
   }
+  // SoA (pi_bin, arbitrary order): count + rank, scan, scatter with the stored ranks
+  if (a.n > 0)
+    k_count_soa<<<grid_for((a.n + 3) / 4, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.x, a.y, a.z, g, a.counts,
+                                                                                 a.rank, a.cell_of, a.ctl);
+  k_scan<false><<<tiles, SCAN_THREADS, 0, s>>>(g.ncells, a.counts, a.offsets, a.tile_status, tiles, a.ctl);
+  if (a.n > 0)
+    k_scatter<false><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
+        a.n, a.x, a.y, a.z, a.q, nullptr, a.id_in, g, a.rank, a.offsets, a.rec_out, a.sid_out, a.perm_out, nullptr,
+        nullptr);
   return cudaGetLastError();
 }
 

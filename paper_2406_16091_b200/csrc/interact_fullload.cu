@@ -259,8 +259,7 @@ __global__ void __launch_bounds__(NT) k_interact_fullload(FlParams p) {
 template <int KERNEL, int NT>
 cudaError_t launch_k(const FlParams &p, cudaStream_t s) {
   const size_t smem = fl_smem_bytes(p.bx, p.by, p.bz, p.cap);
-  cudaError_t e =
-      cudaFuncSetAttribute(k_interact_fullload<KERNEL, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = allow_max_smem(k_interact_fullload<KERNEL, NT>);
   if (e != cudaSuccess) return e;
   const int own = p.g.own_hi - p.g.own_lo;
   dim3 grid((own + p.bx - 1) / p.bx, (p.g.ny + p.by - 1) / p.by, (p.g.nz + p.bz - 1) / p.bz);

@@ -355,7 +355,7 @@ template <int NC>
 cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
   const size_t smem = xp_smem_bytes(p.L, p.capp);
   auto go = [&](auto kern) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = allow_max_smem(kern);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148, occ = 0;
     cudaGetDevice(&dev);

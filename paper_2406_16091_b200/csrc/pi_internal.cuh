@@ -177,6 +177,18 @@ struct InteractArgs {
   int fb[3], fb_cap;            // tuning (full load)
 };
 
+// Lets `func` use the device's whole opt-in shared memory.  The attribute is process-global
+// per function, so it is always set to the same (maximum) value: contexts on other host
+// threads launching with other sizes never see it lowered under them.
+template <typename F>
+inline cudaError_t allow_max_smem(F *func) {
+  int dev = 0, mx = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  return e;
+}
+
 cudaError_t launch_interact_global(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
