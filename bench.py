@@ -31,6 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP32_PEAK_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.45: FMA lanes x SMs x max SM clock
+METRIC = "candidate pair interactions/s (27-cell ordered pairs), step ms"
 WORKLOAD = ("BASELINE configs[1]: 2^21 uniform particles in the unit box, 64^3 cells (8/cell), "
             "r_c = w = 1/64, Gaussian K sigma = r_c/3, fp32")
 
@@ -143,13 +144,39 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+# ------------------------------------------------------------------------ workload (both arms)
+def workload_cloud(a, rank, world):
+    """This rank's synthetic input: configs[1] at N = 1; the X-slab weak-scaling share otherwise."""
+    import synth
+    if world > 1:
+        # rank r owns 64 X layers of a (64 N) x 64 x 64 grid, 8 uniform particles per cell
+        return synth.slab_uniform(8.0, (64, 64, 64), rank, world, seed=synth.SEED_BASE + 1)
+    return synth.make_config(a.config)
+
+
+def workload_config(a, world, cloud, n_total):
+    g = cloud.grid
+    if world > 1:
+        workload = (f"X-slab weak scaling: {g.dims[0]}x{g.dims[1]}x{g.dims[2]} cells (64^3 per GPU), 8 uniform "
+                    f"particles per cell (~2^21 per GPU), r_c = w = 1/64, Gaussian K sigma = r_c/3, fp32; NCCL "
+                    "ghost + migration exchange every step")
+    elif a.config == "c1":
+        workload = WORKLOAD
+    else:
+        workload = f"synth.make_config({a.config!r}): {cloud.n} particles, {tuple(g.dims)} cells, Gaussian K, fp32"
+    return {"workload": workload, "n_per_gpu": cloud.n, "n_total": int(n_total), "cells": g.ncells,
+            "algo": a.algo, "step": "pi_step: bin (count+scan+scatter) + interact + integrate"
+            + (" + a8 migration/ghost exchange (NCCL)" if world > 1 else ""),
+            "l2": "flushed between timed steps (256 MiB write, outside the events)",
+            "parallelism": f"xslab{world}" if world > 1 else "single GPU"}
+
+
 # ------------------------------------------------------------------------ reference arm
 def run_reference(a):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import synth
-    cloud = synth.make_config(a.config)
+    cloud = workload_cloud(a, 0, world)
     cores = host_cores()
     per_step = max(1.0, min(10.0, 120.0 / max(1, a.steps + a.warmup)))
     rates = []
@@ -162,10 +189,10 @@ def run_reference(a):
     unit = "candidate pair interactions/s"
     ms = info["seconds"] * 1e3
     line = {
-        "impl": "reference", "metric": "candidate pair interactions/s (27-cell ordered pairs)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": unit, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": cloud.n, "cells": cloud.grid.ncells},
+        "config": workload_config(a, world, cloud, cloud.n * world),
         "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle",
                          "sample": f"{info['targets']} random targets of the {cloud.n}-particle cloud per step "
                                    f"(fp64 C cell list, OpenMP, {cores} threads; includes its own binning)"},
@@ -190,11 +217,7 @@ def run_ours(a):
         dist.init_process_group("nccl", init_method="env://")
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
-    if world > 1:
-        # X-slab decomposition (a8): rank r owns 64 X layers of a (64 N) x 64 x 64 grid, 8 per cell
-        cloud = synth.slab_uniform(8.0, (64, 64, 64), rank, world, seed=synth.SEED_BASE + 1)
-    else:
-        cloud = synth.make_config(a.config)
+    cloud = workload_cloud(a, rank, world)
     g = cloud.grid
     n = cloud.n
     cap = int(n * 1.25) + 4096 if world > 1 else n  # owned + ghosts + migration slack
@@ -300,17 +323,13 @@ def run_ours(a):
     e2e_value = c_e2e / (e2e_mean * 1e-3)
 
     if world > 1:
-        workload = (f"X-slab weak scaling: {g.dims[0]}x{g.dims[1]}x{g.dims[2]} cells (64^3 per GPU), 8 uniform "
-                    f"particles per cell (~2^21 per GPU, {int(n_all)} total), r_c = w = 1/64, Gaussian K "
-                    "sigma = r_c/3, fp32; NCCL ghost + migration exchange every step")
         # reset, migrate, append, reset, ghosts, append, count, scan, scatter (+ pairify), interact
         launches = 10 + (1 if a.algo == "xpencil" else 0)
     else:
-        workload = WORKLOAD
         # count, scan, scatter, (pairify,) interact (+ integrate fused)
         launches = 4 + (1 if a.algo == "xpencil" else 0)
     line = {
-        "metric": "candidate pair interactions/s (27-cell ordered pairs) and step ms",
+        "metric": METRIC,
         "value": value,
         "unit": "candidate pair interactions/s",
         "n_gpus": world,
@@ -322,12 +341,7 @@ def run_ours(a):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": workload, "n_per_gpu": n, "n_total": int(n_all), "cells": g.ncells,
-                   "algo": a.algo,
-                   "step": "pi_step: bin (count+scan+scatter) + interact + integrate"
-                           + (" + a8 migration/ghost exchange (NCCL)" if world > 1 else ""),
-                   "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "parallelism": f"xslab{world}" if world > 1 else "single GPU"},
+        "config": workload_config(a, world, cloud, n_all),
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic_from_profiles(a.algo),
                      "kernel": f"k_interact_{a.algo}", "flop_per_launch": flop,

@@ -155,6 +155,7 @@ struct pi_ctx_s {
   long long n;       // owned particles (exact on the host when nranks == 1; pi_bin's n otherwise)
   int state;         // 0 empty, 1 binned from pi_bin, 2 sorted state from pi_step (update pending)
   bool need_bin;     // pi_step must re-bin (and, nranks > 1, migrate) first
+  bool pairs_ready;  // c->pairs hold the sorted records as source pairs (written by the AoS scatter)
   bool interacted;
   long long steps;
   SlabState slab;    // nranks > 1
@@ -370,6 +371,8 @@ static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, c
   a.sid_out = c->sid;
   a.perm_out = (rec_in && !perm_in) ? nullptr : c->perm;
   a.perm_in = perm_in;
+  a.pairs_out = rec_in ? c->pairs : nullptr;
+  c->pairs_ready = rec_in != nullptr;
   a.ctl = c->ctl;
   phase_begin(c, 0);
   cudaError_t e = launch_bin(c->g, a, c->stream);
@@ -428,6 +431,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.n_est = multi ? c->n * (long long)(c->slab.Lx + 2) / (c->slab.Lx > 0 ? c->slab.Lx : 1) : c->n;
   a.rec = c->rec;
   a.pairs = c->pairs;
+  a.pairs_ready = c->pairs_ready;
   a.offsets = c->offsets;
   a.ctl = c->ctl;
   a.out.sorted = c->outs;

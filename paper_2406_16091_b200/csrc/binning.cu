@@ -307,7 +307,8 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
                                                             int32_t *__restrict__ sid_out,
                                                             int32_t *__restrict__ perm_out,
                                                             const int32_t *__restrict__ perm_in,
-                                                            const long long *n_dev) {
+                                                            const long long *n_dev,
+                                                            float *__restrict__ pairs_out = nullptr) {
   if (n_dev) n = *n_dev;
   for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
     const long long i = i0 + threadIdx.x;
@@ -332,6 +333,19 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
     }
     int slot = __ldg(offsets + lin) + rk;
     rec_out[slot] = r;
+    if (pairs_out) {  // f32x2 source-pair layout: P[2k] = (x0, x1, y0, y1), P[2k+1] = (z0, z1, q0, q1)
+      float *pp = pairs_out + 8 * (long long)(slot >> 1) + (slot & 1);
+      pp[0] = r.x;
+      pp[2] = r.y;
+      pp[4] = r.z;
+      pp[6] = r.w;
+      if (slot == n - 1 && !(slot & 1)) {  // odd count: an inert partner for the last record
+        pp[1] = 1.0e30f;
+        pp[3] = 1.0e30f;
+        pp[5] = 1.0e30f;
+        pp[7] = 0.f;
+      }
+    }
     sid_out[slot] = id_in ? __ldg(id_in + i) : (int32_t)i;
     if (perm_out) perm_out[slot] = perm_in ? __ldg(perm_in + i) : (int32_t)i;
   }
@@ -358,7 +372,7 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
     if (a.n > 0)
       k_scatter<true, true><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
           a.n, nullptr, nullptr, nullptr, nullptr, a.rec_in, a.id_in, g, a.counts, a.offsets, a.rec_out, a.sid_out,
-          a.perm_out, a.perm_in, a.n_dev);
+          a.perm_out, a.perm_in, a.n_dev, reinterpret_cast<float *>(a.pairs_out));
     return cudaGetLastError();
   }
   // SoA (pi_bin, arbitrary order): count + rank, scan, scatter with the stored ranks

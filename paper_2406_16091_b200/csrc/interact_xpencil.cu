@@ -404,7 +404,7 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   while (xp_smem_bytes(p.L, p.capp) > max_smem && p.capp > 64) p.capp -= 32;
   if (xp_smem_bytes(p.L, p.capp) > max_smem) return cudaErrorNotSupported;
   p.pairs = a.pairs;
-  {
+  if (!a.pairs_ready) {  // the AoS binning (pi_step) writes the pairs itself
     const long long np = (a.n + 1) / 2;
     int blocks = (int)min((np + 255) / 256, 148LL * 16);
     k_pairify<<<max(blocks, 1), 256, 0, s>>>(a.n, a.n_dev, a.rec, a.pairs);

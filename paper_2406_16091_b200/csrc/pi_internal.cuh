@@ -158,6 +158,8 @@ struct BinArgs {
   int32_t *sid_out;             // sorted ids
   int32_t *perm_out;            // sorted slot -> input index (nullable)
   const int32_t *perm_in;       // AoS path: input index per record (-1 = ghost), or NULL
+  float4 *pairs_out;            // AoS path, nullable: also write the sorted records as f32x2
+                                // source pairs (layout of InteractArgs::pairs)
   DevCtl *ctl;
 };
 
@@ -169,7 +171,8 @@ struct InteractArgs {
   const long long *n_dev;       // device-resident count (nranks > 1), or NULL
   long long n_est;              // host estimate of the sorted count (sizes staging buffers)
   const float4 *rec;            // sorted records
-  float4 *pairs;                // scratch [2 * (n / 2 + 1)]: the records as f32x2 source pairs
+  float4 *pairs;                // [2 * (n / 2 + 1)]: the records as f32x2 source pairs
+  bool pairs_ready;             // pairs already hold the current sorted state (AoS binning)
   const int32_t *offsets;       // [ncells + 1]
   OutDesc out;
   DevCtl *ctl;
