@@ -347,7 +347,10 @@ def run_ours(a):
                      "kernel": f"k_interact_{a.algo}", "flop_per_launch": flop,
                      "flop_model": "8 per candidate + 10 per cutoff pair (SURVEY.md §8(d))",
                      "candidates": C, "cutoff_pairs": P, "kernel_ms": int_ms,
-                     "peak_basis": "2 x 128 FP32 lanes x 148 SMs x 1.965 GHz (no FP32 entry in MEASURED_PEAKS)"},
+                     "peak_basis": "2 x 128 FP32 lanes x 148 SMs x 1.965 GHz (no FP32 entry in MEASURED_PEAKS)",
+                     "note": ("effective rate: the unit is the 27-cell candidate pair, but the X-pencil skips "
+                              "the X sub-cells farther than r_c from the target (exact; DESIGN.md R18)"
+                              if a.algo == "xpencil" else "every 27-cell candidate is evaluated")},
         "phases": {"bin_ms": statistics.mean(bin_ms), "interact_ms": int_ms,
                    "exchange_ms": statistics.mean(exch_ms) if world > 1 else 0.0,
                    "migrants_per_step": statistics.mean(migr) if world > 1 else 0.0,

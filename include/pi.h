@@ -104,7 +104,12 @@ typedef struct {
                                 on one rank, broadcast by the caller); NULL iff nranks == 1.
                                 Testing: "PILOCAL:<key>" links the nranks contexts of ONE
                                 process (one host thread per context) without NCCL.          */
-  int32_t reserved[8];       /* must be zero                                                 */
+  int32_t x_subcells;        /* internal X resolution of the binning: inside each cell the
+                                particles are ordered by sub-cell floor(sx (t - c)), t the
+                                contract's scaled coordinate (R18), so the X-pencil
+                                can skip sources farther than r_c along X; 1, 2, 4, 8 or 16
+                                (0 -> 2).  Counts, offsets and M_C stay per cell.            */
+  int32_t reserved[7];       /* must be zero                                                 */
 } pi_config;
 
 typedef struct {

@@ -29,7 +29,7 @@ class PiError(RuntimeError):
 
 
 def _config(dims, cell_width, r_c=None, origin=(0.0, 0.0, 0.0), kernel="gaussian", sigma=0.0, capacity=0,
-            rank=0, nranks=1):
+            rank=0, nranks=1, x_subcells=0):
     cfg = L.pi_config()
     for a in range(3):
         cfg.origin[a] = float(origin[a])
@@ -41,6 +41,7 @@ def _config(dims, cell_width, r_c=None, origin=(0.0, 0.0, 0.0), kernel="gaussian
     cfg.capacity = int(capacity)
     cfg.rank = int(rank)
     cfg.nranks = int(nranks)
+    cfg.x_subcells = int(x_subcells)
     return cfg
 
 
@@ -83,14 +84,15 @@ class Context:
     """
 
     def __init__(self, dims, cell_width, r_c=None, origin=(0.0, 0.0, 0.0), kernel="gaussian", sigma=0.0,
-                 capacity=0, device=None, stream=None, rank=0, nranks=1, nccl_unique_id=None):
+                 capacity=0, device=None, stream=None, rank=0, nranks=1, nccl_unique_id=None, x_subcells=0):
         self._lib = L.load()
         self.device = torch.device(device if device is not None else "cuda")
         self.dims = tuple(int(d) for d in dims)
         self.cell_width = float(cell_width)
         self.r_c = float(cell_width if r_c is None else r_c)
         self.origin = tuple(float(o) for o in origin)
-        cfg = _config(self.dims, self.cell_width, self.r_c, self.origin, kernel, sigma, capacity, rank, nranks)
+        cfg = _config(self.dims, self.cell_width, self.r_c, self.origin, kernel, sigma, capacity, rank, nranks,
+                      x_subcells)
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         self.stream = stream

@@ -20,7 +20,8 @@ class pi_config(ctypes.Structure):
     _fields_ = [("origin", ctypes.c_float * 3), ("cell_width", ctypes.c_float), ("dims", ctypes.c_int32 * 3),
                 ("r_c", ctypes.c_float), ("kernel", ctypes.c_int32), ("kparam", ctypes.c_float * 4),
                 ("capacity", ctypes.c_int64), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32),
-                ("nranks", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 8)]
+                ("nranks", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p), ("x_subcells", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 7)]
 
 
 class pi_stats(ctypes.Structure):

@@ -18,7 +18,7 @@ constexpr size_t ALIGN = 256;
 size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-  size_t ctl, counts, offsets, tiles, rec, sid, perm, urec, uid, rank, outs, io, pairs;
+  size_t ctl, counts, offsets, foffsets, tiles, rec, sid, perm, urec, uid, rank, outs, io, pairs;
   size_t xrec, xid, xperm, msg[4];  // nranks > 1
   size_t total;
 };
@@ -53,6 +53,8 @@ SlabGeom slab_geom(const pi_config *cfg) {
   return s;
 }
 
+int x_subcells(const pi_config *cfg) { return cfg->x_subcells > 0 ? cfg->x_subcells : 2; }
+
 Layout make_layout(const pi_config *cfg) {
   const SlabGeom sg = slab_geom(cfg);
   const long long ncells = sg.ncells_local;
@@ -64,10 +66,12 @@ Layout make_layout(const pi_config *cfg) {
     o = align_up(o + bytes);
     return at;
   };
+  const long long nf = ncells * x_subcells(cfg);  // fine (X sub-cell) bins
   L.ctl = take(sizeof(DevCtl));
-  L.counts = take(sizeof(int32_t) * (size_t)(ncells + 4));
+  L.counts = take(sizeof(int32_t) * (size_t)(nf + 4));
   L.offsets = take(sizeof(int32_t) * (size_t)(ncells + 4));
-  L.tiles = take(sizeof(unsigned long long) * (size_t)scan_tiles(ncells));
+  L.foffsets = take(sizeof(int32_t) * (size_t)(nf + 4));
+  L.tiles = take(sizeof(unsigned long long) * (size_t)scan_tiles(nf));
   L.rec = take(sizeof(float4) * (size_t)cap);
   L.sid = take(sizeof(int32_t) * (size_t)cap);
   L.perm = take(sizeof(int32_t) * (size_t)cap);
@@ -148,7 +152,7 @@ struct pi_ctx_s {
   Layout lay;
   unsigned char *ws;
   DevCtl *ctl;
-  int32_t *counts, *offsets, *sid, *perm, *uid, *rank;
+  int32_t *counts, *offsets, *foffsets, *sid, *perm, *uid, *rank;
   unsigned long long *tiles;
   float4 *rec, *urec, *outs, *pairs;
   float *io;
@@ -196,6 +200,10 @@ static bool config_ok(const pi_config *cfg, char *why, size_t n) {
   if (cfg->capacity < 0 || cfg->capacity > (1LL << 31) - 64) { snprintf(why, n, "capacity out of range"); return false; }
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) { snprintf(why, n, "bad rank/nranks"); return false; }
   if (cfg->dims[0] % cfg->nranks) { snprintf(why, n, "dims[0] must be divisible by nranks"); return false; }
+  if (cfg->x_subcells < 0 || cfg->x_subcells > 16 || (cfg->x_subcells & (cfg->x_subcells - 1))) {
+    snprintf(why, n, "x_subcells must be 0 or a power of two <= 16");
+    return false;
+  }
   if (cfg->nranks > 1 && !cfg->nccl_unique_id) { snprintf(why, n, "nranks > 1 needs nccl_unique_id"); return false; }
   long long nc = (long long)cfg->dims[0] * cfg->dims[1] * cfg->dims[2];
   if (nc > (1LL << 30)) { snprintf(why, n, "too many cells"); return false; }
@@ -251,6 +259,7 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   c->ctl = reinterpret_cast<DevCtl *>(c->ws + lay.ctl);
   c->counts = reinterpret_cast<int32_t *>(c->ws + lay.counts);
   c->offsets = reinterpret_cast<int32_t *>(c->ws + lay.offsets);
+  c->foffsets = reinterpret_cast<int32_t *>(c->ws + lay.foffsets);
   c->tiles = reinterpret_cast<unsigned long long *>(c->ws + lay.tiles);
   c->rec = reinterpret_cast<float4 *>(c->ws + lay.rec);
   c->sid = reinterpret_cast<int32_t *>(c->ws + lay.sid);
@@ -272,6 +281,7 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   g.gx_off = sg.gx_off;
   g.own_lo = sg.own_lo;
   g.own_hi = sg.own_hi;
+  g.sx = x_subcells(cfg);
   g.lx = g.ox; g.ly = g.oy; g.lz = g.oz;
   g.hx = g.ox + (float)cfg->dims[0] * g.w;
   g.hy = g.oy + (float)g.ny * g.w;
@@ -366,6 +376,7 @@ static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, c
   a.rank = c->rank;
   a.counts = c->counts;
   a.offsets = c->offsets;
+  a.foffsets = c->foffsets;
   a.tile_status = c->tiles;
   a.rec_out = c->rec;
   a.sid_out = c->sid;
@@ -430,6 +441,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.n_dev = multi ? &c->ctl->n_total : nullptr;
   a.n_est = multi ? c->n * (long long)(c->slab.Lx + 2) / (c->slab.Lx > 0 ? c->slab.Lx : 1) : c->n;
   a.rec = c->rec;
+  a.foffsets = c->foffsets;
   a.pairs = c->pairs;
   a.pairs_ready = c->pairs_ready;
   a.offsets = c->offsets;

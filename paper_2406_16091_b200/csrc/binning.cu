@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_count_soa(long long n, const 
     for (int j = 0; j < 4; ++j) {
       bool ok = in && i0 + j < n;
       bool b = false;
-      lin[j] = cell_lin(g, xs[j], ys[j], zs[j], b);
+      lin[j] = fine_lin(g, xs[j], ys[j], zs[j], b);
       bad |= ok && b;
       rk[j] = agg_increment(counts, lin[j], ok);
     }
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_count_aos(long long n, const 
     const bool ok = i < n;
     const float4 r = ok ? __ldg(rec + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     bool b = false;
-    const int lin = cell_lin(g, r.x, r.y, r.z, b);
+    const int lin = fine_lin(g, r.x, r.y, r.z, b);
     bad |= ok && b;
     run_count(counts, lin, ok);
   }
@@ -164,11 +164,14 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
   return v;
 }
 
+// The scan runs over the FINE counts (X sub-cells, sx per cell; sx divides SCAN_ITEMS, so a
+// thread's items are whole cells): it writes the fine offsets (the sorted order) and every
+// sx-th of them as the per-cell offsets; M_C is the largest per-cell sum.
 template <bool KEEP>  // KEEP: leave the counts (the scatter consumes them)
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t *__restrict__ counts,
                                                        int32_t *__restrict__ offsets,
                                                        unsigned long long *__restrict__ status, int num_tiles,
-                                                       DevCtl *ctl) {
+                                                       DevCtl *ctl, int sx, int32_t *__restrict__ cell_offsets) {
   __shared__ int s_tile;
   __shared__ int s_warp[SCAN_THREADS / 32];
   __shared__ int s_prefix;
@@ -200,9 +203,16 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
       if (!KEEP && c < ncells) counts[c] = 0;
     }
   }
-  int mx = 0, sum = 0;
+  int mx = 0, sum = 0, grp = 0;
 #pragma unroll
-  for (int k = 0; k < SCAN_ITEMS; ++k) { mx = max(mx, v[k]); sum += v[k]; }
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    sum += v[k];
+    grp += v[k];
+    if ((k + 1) % sx == 0) {  // end of a cell
+      mx = max(mx, grp);
+      grp = 0;
+    }
+  }
   // warp inclusive scan of the thread sums
   int incl = sum;
 #pragma unroll
@@ -272,7 +282,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
     for (int k = 0; k < SCAN_ITEMS; ++k)
       if (base + k < ncells) offsets[base + k] = outv[k];
   }
-  if (base <= ncells - 1 && ncells - 1 < base + SCAN_ITEMS) offsets[ncells] = run;  // offsets[Nc] = N
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; k += 1)  // per-cell offsets: every sx-th fine offset
+    if (k % sx == 0 && base + k < ncells) cell_offsets[(base + k) / sx] = outv[k];
+  if (base <= ncells - 1 && ncells - 1 < base + SCAN_ITEMS) {  // offsets[Nc] = N
+    offsets[ncells] = run;
+    cell_offsets[ncells / sx] = run;
+  }
   // last block: publish M_C, reset counters, advance the epoch
   __syncthreads();
   if (tid == 0) {
@@ -323,7 +339,7 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
       }
     }
     bool b = false;
-    int lin = cell_lin(g, r.x, r.y, r.z, b);
+    int lin = fine_lin(g, r.x, r.y, r.z, b);
     int rk;
     if (TAKE) {
       rk = run_take(const_cast<int32_t *>(rank), lin, ok);  // rank = the counts array here
@@ -331,7 +347,7 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
     } else {
       rk = __ldg(rank + i);
     }
-    int slot = __ldg(offsets + lin) + rk;
+    int slot = __ldg(offsets + lin) + rk;  // fine offsets
     rec_out[slot] = r;
     if (pairs_out) {  // f32x2 source-pair layout: P[2k] = (x0, x1, y0, y1), P[2k+1] = (z0, z1, q0, q1)
       float *pp = pairs_out + 8 * (long long)(slot >> 1) + (slot & 1);
@@ -361,17 +377,19 @@ int grid_for(long long work, int threads) {
 
 }  // namespace
 
-int scan_tiles(long long ncells) { return (int)((ncells + SCAN_TILE - 1) / SCAN_TILE); }
+int scan_tiles(long long nitems) { return (int)((nitems + SCAN_TILE - 1) / SCAN_TILE); }
 
 cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
-  const int tiles = scan_tiles(g.ncells);
+  const long long nf = g.ncells * g.sx;  // fine cells
+  const int tiles = scan_tiles(nf);
   if (a.rec_in) {  // AoS: count, scan keeping the counts, scatter taking ranks from them
     if (a.n > 0)
       k_count_aos<<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.rec_in, g, a.counts, a.ctl, a.n_dev);
-    k_scan<true><<<tiles, SCAN_THREADS, 0, s>>>(g.ncells, a.counts, a.offsets, a.tile_status, tiles, a.ctl);
+    k_scan<true><<<tiles, SCAN_THREADS, 0, s>>>(nf, a.counts, a.foffsets, a.tile_status, tiles, a.ctl, g.sx,
+                                                a.offsets);
     if (a.n > 0)
       k_scatter<true, true><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
-          a.n, nullptr, nullptr, nullptr, nullptr, a.rec_in, a.id_in, g, a.counts, a.offsets, a.rec_out, a.sid_out,
+          a.n, nullptr, nullptr, nullptr, nullptr, a.rec_in, a.id_in, g, a.counts, a.foffsets, a.rec_out, a.sid_out,
           a.perm_out, a.perm_in, a.n_dev, reinterpret_cast<float *>(a.pairs_out));
     return cudaGetLastError();
   }
@@ -379,10 +397,11 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
   if (a.n > 0)
     k_count_soa<<<grid_for((a.n + 3) / 4, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.x, a.y, a.z, g, a.counts,
                                                                                  a.rank, a.cell_of, a.ctl);
-  k_scan<false><<<tiles, SCAN_THREADS, 0, s>>>(g.ncells, a.counts, a.offsets, a.tile_status, tiles, a.ctl);
+  k_scan<false><<<tiles, SCAN_THREADS, 0, s>>>(nf, a.counts, a.foffsets, a.tile_status, tiles, a.ctl, g.sx,
+                                                 a.offsets);
   if (a.n > 0)
     k_scatter<false><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
-        a.n, a.x, a.y, a.z, a.q, nullptr, a.id_in, g, a.rank, a.offsets, a.rec_out, a.sid_out, a.perm_out, nullptr,
+        a.n, a.x, a.y, a.z, a.q, nullptr, a.id_in, g, a.rank, a.foffsets, a.rec_out, a.sid_out, a.perm_out, nullptr,
         nullptr);
   return cudaGetLastError();
 }

@@ -49,36 +49,43 @@ struct XpParams {
   const float4 *rec;
   const float4 *pairs;  // the sorted records as f32x2 source pairs (k_pairify)
   const int32_t *offsets;
+  const int32_t *foffsets;  // fine offsets: sx X sub-cells per cell (the sorted order)
   Geom g;
   KParams kp;
   OutDesc out;
   DevCtl *ctl;
   int L;             // target cells per work item along X (segment length)
+  int sx;            // X sub-cells per cell
+  bool mask;         // mask the out-of-run halves of a run's end pairs (walk9)
   int capp;          // staged source pairs per slot
   int nseg;          // segments per X row
   long long nitems;  // rows x segments
 };
 
-// Slot: S[2 capp] float4 (source pairs) | meta[16] | O[9][L+3] | rb[16]
-//   O[r][j]  global offsets of pencil r (= (dy + 1) + 3 (dz + 1)) at cell boundary x0-1+j
+// Slot: S[2 capp] float4 (source pairs) | meta[16] | O[9][LF] | rb[16],  LF = (L+2) sx + 1
+//   O[r][k]  global offsets of pencil r (= (dy + 1) + 3 (dz + 1)) at the fine (X sub-cell)
+//            boundary k of the cells x0-1 .. x0+L; the cell boundary j is O[r][j sx]
 //   rb[r]    first staged pair of pencil r's run in S (rb[9] = total)
 // meta: 0 stop (1), 1 ja, 2 jb (target cells ja..jb of the item in this round; jb < ja: the
 //       global-memory fallback for cell ja), 3 ntargets, 4 x0, 5 cy | cz << 16, 6 batch counter
-__host__ __device__ inline int slot_words(int L) { return (META + 9 * (L + 3) + 16 + 3) & ~3; }
-__host__ __device__ inline size_t slot_bytes(int L, int capp) { return (size_t)capp * 32 + (size_t)slot_words(L) * 4; }
-__host__ __device__ inline size_t xp_smem_bytes(int L, int capp) { return 128 + NSLOT * slot_bytes(L, capp); }
+__host__ __device__ inline int lf_of(int L, int sx) { return (L + 2) * sx + 1; }
+__host__ __device__ inline int slot_words(int L, int sx) { return (META + 9 * lf_of(L, sx) + 16 + 3) & ~3; }
+__host__ __device__ inline size_t slot_bytes(int L, int capp, int sx) {
+  return (size_t)capp * 32 + (size_t)slot_words(L, sx) * 4;
+}
+__host__ __device__ inline size_t xp_smem_bytes(int L, int capp, int sx) { return 128 + NSLOT * slot_bytes(L, capp, sx); }
 
 struct Slot {
   float4 *S;
   int *meta, *O, *rb;
 };
-__device__ __forceinline__ Slot slot_at(unsigned char *base, int L, int capp, int s) {
-  unsigned char *u = base + (size_t)s * slot_bytes(L, capp);
+__device__ __forceinline__ Slot slot_at(unsigned char *base, int L, int capp, int sx, int s) {
+  unsigned char *u = base + (size_t)s * slot_bytes(L, capp, sx);
   Slot sl;
   sl.S = reinterpret_cast<float4 *>(u);
   sl.meta = reinterpret_cast<int *>(u + (size_t)capp * 32);
   sl.O = sl.meta + META;
-  sl.rb = sl.O + 9 * (L + 3);
+  sl.rb = sl.O + 9 * lf_of(L, sx);
   return sl;
 }
 
@@ -101,11 +108,12 @@ __global__ void k_pairify(long long n, const long long *n_dev, const float4 *__r
 }
 
 // ---------------------------------------------------------------- producer (one warp)
-// Offsets of the 9 pencils of `item` at the cell boundaries x0-1 .. x0+L+1 into the slot.
+// Fine offsets of the 9 pencils of `item` at the X sub-cell boundaries of cells x0-1 .. x0+L
+// (clamped: cells outside the grid are empty).
 __device__ void load_offsets(const XpParams &p, const Slot &sl, long long item, int &x0, int &Lseg, int &cy,
                              int &cz) {
   const int lane = threadIdx.x & 31;
-  const int L3 = p.L + 3;
+  const int LF = lf_of(p.L, p.sx), sx = p.sx;
   const Geom &g = p.g;
   const int seg = (int)(item % p.nseg);
   const long long row = item / p.nseg;
@@ -113,20 +121,21 @@ __device__ void load_offsets(const XpParams &p, const Slot &sl, long long item, 
   cz = (int)(row / g.ny);
   x0 = g.own_lo + seg * p.L;  // owned X cells only (ghost layers are staged as sources)
   Lseg = min(p.L, g.own_hi - x0);
-  for (int j0 = 0; j0 < L3; j0 += 32) {
-    const int j = j0 + lane;
-    const int x = min(max(x0 - 1 + j, 0), g.nx);  // clamped: cells outside the grid are empty
+  const int nxf = g.nx * sx;
+  for (int k0 = 0; k0 < LF; k0 += 32) {
+    const int k = k0 + lane;
+    const int bf = min(max((x0 - 1) * sx + k, 0), nxf);
     int v[9];
 #pragma unroll
     for (int r = 0; r < 9; ++r) {
       const int y = cy + (r % 3) - 1, z = cz + (r / 3) - 1;
       v[r] = 0;
-      if (j < L3 && y >= 0 && y < g.ny && z >= 0 && z < g.nz)
-        v[r] = __ldg(p.offsets + (long long)g.nx * (y + (long long)g.ny * z) + x);
+      if (k < LF && y >= 0 && y < g.ny && z >= 0 && z < g.nz)
+        v[r] = __ldg(p.foffsets + (long long)nxf * (y + (long long)g.ny * z) + bf);
     }
-    if (j < L3) {
+    if (k < LF) {
 #pragma unroll
-      for (int r = 0; r < 9; ++r) sl.O[r * L3 + j] = v[r];
+      for (int r = 0; r < 9; ++r) sl.O[r * LF + k] = v[r];
     }
   }
   __syncwarp();
@@ -136,14 +145,15 @@ __device__ void load_offsets(const XpParams &p, const Slot &sl, long long item, 
 // whole source pairs) fit the slot (warp-uniform; jb < ja: cell ja alone does not fit).
 __device__ int choose_round(const XpParams &p, const Slot &sl, int ja, int Lseg) {
   const int lane = threadIdx.x & 31;
-  const int L3 = p.L + 3;
+  const int LF = lf_of(p.L, p.sx), sx = p.sx;
   int jb = ja - 1;
   for (int j0 = ja; j0 <= Lseg; j0 += 32) {
     const int j = j0 + lane;
     int tot = 0;
     if (j <= Lseg) {
 #pragma unroll
-      for (int r = 0; r < 9; ++r) tot += ((sl.O[r * L3 + j + 2] + 1) >> 1) - (sl.O[r * L3 + ja - 1] >> 1);
+      for (int r = 0; r < 9; ++r)
+        tot += ((sl.O[r * LF + (j + 2) * sx] + 1) >> 1) - (sl.O[r * LF + (ja - 1) * sx] >> 1);
     }
     const unsigned b = __ballot_sync(0xffffffffu, j <= Lseg && tot <= p.capp);
     jb += __popc(b);
@@ -153,22 +163,39 @@ __device__ int choose_round(const XpParams &p, const Slot &sl, int ja, int Lseg)
 }
 
 // ---------------------------------------------------------------- consumer
-// (phi, sum w d) of the target `me` over the 9 runs of cell j (cells j-1 .. j+1 of every
-// pencil).  A run [a, b) of records covers the staged pairs a/2 .. (b-1)/2; the halves of its
-// first and last pair that lie outside the run get q = 0 (they add exactly 0).  The self
-// term (= q_t exactly: d = 0, K(0) = 2^0 = 1) is removed.
-template <int KERNEL>
-__device__ __forceinline__ float4 walk9(const Slot &sl, int L3, int ja, int j, const float4 me, const float thr,
-                                        const float mc2) {
+// (phi, sum w d) of the target `me` over its 9 runs: fine boundaries klo .. khi+1 of every
+// pencil (inside cells j-1 .. j+1: the X sub-cells that can hold a source closer than r_c
+// along X).  A run [a, b) of records covers the staged pairs a/2 .. (b-1)/2.  The halves of
+// its first and last pair outside the run are the records a-1 and b of the sorted array:
+//   MASK = true  (CANDIDATE kernel, or grids under 4 cells along X): they get q = 0;
+//   MASK = false (cutoff kernels): they are evaluated as they are -- record a-1 lies in a
+//     skipped sub-cell or cell of the same pencil (|dx| >= r_c by construction) or, at a row
+//     start, in the last cell of the previous row (|dx| > (nx - 3) w >= r_c), and likewise
+//     record b, or b is the inert partner after the last record -- so r^2 >= r_c^2 in fp32 too
+//     and they add exactly 0; no peeled iterations.
+// The self term (= q_t exactly: d = 0, K(0) = 2^0 = 1) is removed.
+template <int KERNEL, bool MASK>
+__device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, int klo, int khi, const float4 me,
+                                        const float thr, const float mc2) {
   const float4 *__restrict__ S = sl.S;
   p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
   p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
 #pragma unroll 1
   for (int r = 0; r < 9; ++r) {
-    const int a = sl.O[r * L3 + j - 1], b = sl.O[r * L3 + j + 2];
+    const int a = sl.O[r * LF + klo], b = sl.O[r * LF + khi + 1];
     if (b <= a) continue;
-    const int base = sl.rb[r] - (sl.O[r * L3 + ja - 1] >> 1);
+    const int base = sl.rb[r] - (sl.O[r * LF + (ja - 1) * sx] >> 1);
     const int p0 = base + (a >> 1), pl = base + ((b - 1) >> 1);  // first and last pair
+    if (!MASK) {
+      int q = p0;
+      for (; q + 1 <= pl; q += 2) {
+        const SrcPair s0 = load_pair(S, q), s1 = load_pair(S, q + 1);
+        src_eval<KERNEL>(s0, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz);
+        src_eval<KERNEL>(s1, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb);
+      }
+      if (q <= pl) src_eval<KERNEL>(load_pair(S, q), me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz);
+      continue;
+    }
     {
       SrcPair f = load_pair(S, p0);
       f.q = pk((a & 1) ? 0.f : lo(f.q), (p0 == pl && (b & 1)) ? 0.f : hi(f.q));
@@ -201,7 +228,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem_raw);  // [NSLOT]
   unsigned long long *empty = full + NSLOT;                                      // [NSLOT]
   unsigned char *slots = smem_raw + 128;
-  const int L = p.L, L3 = L + 3;
+  const int L = p.L, sx = p.sx, LF = lf_of(L, sx);
   const Geom &g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned long long cand = 0, fallbacks = 0;
@@ -221,7 +248,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     int x0 = 0, Lseg = 0, cy = 0, cz = 0, ja = 1;
     for (unsigned use = 0;; ++use) {
       const int s = use % NSLOT;
-      const Slot sl = slot_at(slots, L, p.capp, s);
+      const Slot sl = slot_at(slots, L, p.capp, sx, s);
       XP_T(t0);
       if (use >= NSLOT) mbar_wait(&empty[s], ((use / NSLOT) - 1) & 1);  // consumers released it
       XP_T(t1);
@@ -241,8 +268,8 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         ja = 1;
       } else {
         // next round of the same item: the offsets are reused (copy them into this slot)
-        const Slot prev = slot_at(slots, L, p.capp, (use - 1) % NSLOT);
-        for (int k = lane; k < 9 * L3; k += 32) sl.O[k] = prev.O[k];
+        const Slot prev = slot_at(slots, L, p.capp, sx, (use - 1) % NSLOT);
+        for (int k = lane; k < 9 * LF; k += 32) sl.O[k] = prev.O[k];
         __syncwarp();
       }
       const int jb = choose_round(p, sl, ja, Lseg);
@@ -250,8 +277,8 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       const int last = jb < ja ? ja : jb;
       int a = 0, len = 0;  // pairs of pencil run `lane`
       if (lane < 9) {
-        a = sl.O[lane * L3 + ja - 1] >> 1;
-        len = jb < ja ? 0 : ((sl.O[lane * L3 + last + 2] + 1) >> 1) - a;
+        a = sl.O[lane * LF + (ja - 1) * sx] >> 1;
+        len = jb < ja ? 0 : ((sl.O[lane * LF + (last + 2) * sx] + 1) >> 1) - a;
       }
       int incl = len;
 #pragma unroll
@@ -266,7 +293,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         sl.meta[0] = 0;
         sl.meta[1] = ja;
         sl.meta[2] = jb;
-        sl.meta[3] = sl.O[4 * L3 + last + 1] - sl.O[4 * L3 + ja];
+        sl.meta[3] = sl.O[4 * LF + (last + 1) * sx] - sl.O[4 * LF + ja * sx];
         sl.meta[4] = x0;
         sl.meta[5] = cy | (cz << 16);
         sl.meta[6] = 0;
@@ -285,7 +312,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     const float thr = p.kp.rc2, mc2 = -p.kp.c2;
     for (unsigned use = 0;; ++use) {
       const int s = use % NSLOT;
-      const Slot sl = slot_at(slots, L, p.capp, s);
+      const Slot sl = slot_at(slots, L, p.capp, sx, s);
       XP_T(c0);
       mbar_wait(&full[s], (use / NSLOT) & 1);
       XP_T(c1);
@@ -293,8 +320,11 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       if (sl.meta[0]) break;  // out of work items
       const int ja = sl.meta[1], jb = sl.meta[2], ntargets = sl.meta[3], x0 = sl.meta[4];
       const int cy = sl.meta[5] & 0xffff, cz = sl.meta[5] >> 16;
-      const int *O4 = sl.O + 4 * L3;
-      const int t0 = O4[ja];  // global sorted index of the round's first target
+      const int *O4 = sl.O + 4 * LF;  // home pencil; cell boundary j at O4[j sx]
+      const int t0 = O4[ja * sx];       // global sorted index of the round's first target
+      // global fine X index of the item's cell 0 (fine boundaries of the tables start there)
+      const int f0 = (x0 - 1 + g.gx_off) * sx;
+      const float rc = p.kp.rc;
       for (;;) {
         int b = 0;
         if (lane == 0) b = atomicAdd(&sl.meta[6], 32);
@@ -307,20 +337,30 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
             fallback_target<KERNEL>(gs, x0 - 1 + ja, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand);
             if (T == 0) ++fallbacks;
           } else {
-            // cell of the target: last j in [ja, jb] with O4[j] <= gs
+            // cell of the target: last j in [ja, jb] with O4[j sx] <= gs
             int lo_ = ja, hi_ = jb;
             while (lo_ < hi_) {
               const int mid = (lo_ + hi_ + 1) >> 1;
-              if (O4[mid] <= gs) lo_ = mid; else hi_ = mid - 1;
+              if (O4[mid * sx] <= gs) lo_ = mid; else hi_ = mid - 1;
             }
             const int j = lo_;
-            const int tp = sl.rb[4] - (sl.O[4 * L3 + ja - 1] >> 1) + (gs >> 1);  // the target's pair
+            const int tp = sl.rb[4] - (O4[(ja - 1) * sx] >> 1) + (gs >> 1);  // the target's pair
             const float4 ua = sl.S[2 * tp], ub = sl.S[2 * tp + 1];
             const float4 me = (gs & 1) ? make_float4(ua.y, ua.w, ub.y, ub.w) : make_float4(ua.x, ua.z, ub.x, ub.z);
-            const float4 r = walk9<KERNEL>(sl, L3, ja, j, me, thr, mc2);
-            int nc = 0;
+            // X sub-cells that can hold a source with |x_s - x_t| < r_c: the fine index is
+            // monotone in x, and x_t - r_c / x_t + r_c are rounded outward, so every skipped
+            // source has |dx| >= r_c exactly (reading R18)
+            bool bad = false;
+            const int flo = fine_x_global(g, __fsub_rd(me.x, rc), bad) - f0;
+            const int fhi = fine_x_global(g, __fadd_ru(me.x, rc), bad) - f0;
+            // (the CANDIDATE test kernel counts every candidate: no pruning)
+            const int klo = KERNEL == PI_K_CANDIDATE ? (j - 1) * sx : min(max(flo, (j - 1) * sx), (j + 2) * sx - 1);
+            const int khi = KERNEL == PI_K_CANDIDATE ? (j + 2) * sx - 1 : min(max(fhi, (j - 1) * sx), (j + 2) * sx - 1);
+            const float4 r = p.mask ? walk9<KERNEL, true>(sl, LF, sx, ja, klo, khi, me, thr, mc2)
+                                    : walk9<KERNEL, false>(sl, LF, sx, ja, klo, khi, me, thr, mc2);
+            int nc = 0;  // the 27-cell candidates (the unit of the metric, R4), pruned or not
 #pragma unroll
-            for (int rr = 0; rr < 9; ++rr) nc += sl.O[rr * L3 + j + 2] - sl.O[rr * L3 + j - 1];
+            for (int rr = 0; rr < 9; ++rr) nc += sl.O[rr * LF + (j + 2) * sx] - sl.O[rr * LF + (j - 1) * sx];
             cand += (unsigned long long)(nc - 1);
             if (KERNEL == PI_K_GAUSSIAN) {
               const float sc = -me.w * p.kp.inv_s2;
@@ -353,7 +393,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
 
 template <int NC>
 cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
-  const size_t smem = xp_smem_bytes(p.L, p.capp);
+  const size_t smem = xp_smem_bytes(p.L, p.capp, p.sx);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(kern);
     if (e != cudaSuccess) return e;
@@ -392,6 +432,9 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   if (p.L > own) p.L = own;
   p.nseg = (own + p.L - 1) / p.L;
   p.nitems = (long long)p.nseg * g.ny * g.nz;
+  p.foffsets = a.foffsets;
+  p.sx = g.sx;
+  p.mask = k.kernel == PI_K_CANDIDATE || g.nx < 4;
   const int nc = a.threads > 0 ? a.threads / 32 : 20;
   int cap = a.tx_cap;
   if (cap <= 0) {
@@ -401,8 +444,8 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   }
   p.capp = max(16, cap / 2 + 9);  // + one partial pair per run
   const size_t max_smem = 227 * 1024;
-  while (xp_smem_bytes(p.L, p.capp) > max_smem && p.capp > 64) p.capp -= 32;
-  if (xp_smem_bytes(p.L, p.capp) > max_smem) return cudaErrorNotSupported;
+  while (xp_smem_bytes(p.L, p.capp, p.sx) > max_smem && p.capp > 64) p.capp -= 32;
+  if (xp_smem_bytes(p.L, p.capp, p.sx) > max_smem) return cudaErrorNotSupported;
   p.pairs = a.pairs;
   if (!a.pairs_ready) {  // the AoS binning (pi_step) writes the pairs itself
     const long long np = (a.n + 1) / 2;

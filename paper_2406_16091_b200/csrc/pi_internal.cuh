@@ -18,6 +18,7 @@ struct Geom {
   int gnx;            // global dims[0]
   int gx_off;         // global X index of local X cell 0 (-1 + rank * Lx when nranks > 1)
   int own_lo, own_hi; // owned local X cells [own_lo, own_hi): targets of the interaction
+  int sx;             // X sub-cells per cell of the binning order (1, 2, 4, 8, 16)
   float hx, hy, hz;   // upper faces of the global box (integration walls)
   float lx, ly, lz;   // lower faces
 };
@@ -78,6 +79,29 @@ __device__ __forceinline__ int cell_lin(const Geom &g, float x, float y, float z
   int cy = cell_coord(y, g.oy, g.inv_w, g.ny, bad);
   int cz = cell_coord(z, g.oz, g.inv_w, g.nz, bad);
   return cx + g.nx * (cy + g.ny * cz);
+}
+
+// Fine (sub-cell) X index on the GLOBAL grid: c sx + floor(sx (t - c)), t = fl32(fl32(x - o)
+// inv_w) the contract's scaled coordinate and c its cell.  t - c is exact (t in [c, c+1)) and
+// sx a power of two, so the index is monotone in x and agrees with the cell contract.
+__device__ __forceinline__ int fine_x_global(const Geom &g, float x, bool &bad) {
+  const float t = __fmul_rn(__fsub_rn(x, g.ox), g.inv_w);
+  const float f = floorf(t);
+  bad |= !(f == f);
+  const int c = (f >= 0.f) ? ((f < (float)g.gnx) ? (int)f : g.gnx - 1) : 0;
+  const int sub = min(max((int)((t - (float)c) * (float)g.sx), 0), g.sx - 1);
+  return c * g.sx + sub;
+}
+
+// Linear FINE cell (the binning order): X sub-cell fastest inside the cell, then the cell
+// linearisation; cells outside the local slab clamp into the ghost layers like cell_lin.
+__device__ __forceinline__ int fine_lin(const Geom &g, float x, float y, float z, bool &bad) {
+  const int fg = fine_x_global(g, x, bad);
+  const int cl = fg / g.sx - g.gx_off;
+  const int fx = cl < 0 ? 0 : (cl >= g.nx ? g.nx * g.sx - 1 : cl * g.sx + (fg - (fg / g.sx) * g.sx));
+  const int cy = cell_coord(y, g.oy, g.inv_w, g.ny, bad);
+  const int cz = cell_coord(z, g.oz, g.inv_w, g.nz, bad);
+  return fx + g.nx * g.sx * (cy + g.ny * cz);
 }
 
 __device__ __forceinline__ float ex2_approx(float a) {
@@ -150,8 +174,9 @@ struct BinArgs {
   const int32_t *id_in;         // ids (NULL -> index)
   int32_t *cell_of;             // optional: a1 output in input order
   int32_t *rank;                // scratch [n]
-  int32_t *counts;              // [ncells], zero on entry, zeroed again by the scan
-  int32_t *offsets;             // [ncells + 1]
+  int32_t *counts;              // [ncells sx] fine counts, zero on entry and again after the binning
+  int32_t *offsets;             // [ncells + 1] per cell
+  int32_t *foffsets;            // [ncells sx + 1] per fine cell (the sorted order)
   unsigned long long *tile_status;
   int num_tiles_cap;
   float4 *rec_out;              // sorted records (x, y, z, q)
@@ -164,7 +189,7 @@ struct BinArgs {
 };
 
 cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s);
-int scan_tiles(long long ncells);
+int scan_tiles(long long nitems);
 
 struct InteractArgs {
   long long n;                  // particles in the sorted state (upper bound if n_dev)
@@ -174,6 +199,7 @@ struct InteractArgs {
   float4 *pairs;                // [2 * (n / 2 + 1)]: the records as f32x2 source pairs
   bool pairs_ready;             // pairs already hold the current sorted state (AoS binning)
   const int32_t *offsets;       // [ncells + 1]
+  const int32_t *foffsets;      // [ncells sx + 1] fine offsets (X sub-cells)
   OutDesc out;
   DevCtl *ctl;
   int tx_len, tx_cap, threads, groups;  // tuning (x-pencil)
