@@ -71,6 +71,14 @@ def test_workspace_bytes_validation(lib):
     assert lib.pi_workspace_bytes(ctypes.byref(_cfg(dims=(0, 16, 16)))) == 0
     assert lib.pi_workspace_bytes(ctypes.byref(_cfg(nranks=3, dims=(16, 16, 16)))) == 0
     assert lib.pi_workspace_bytes(None) == 0
+    # x_subcells: 0 (default) or a power of two <= 16; finer X order needs more fine offsets
+    c1, c8 = _cfg(), _cfg()
+    c1.x_subcells, c8.x_subcells = 1, 8
+    assert 0 < lib.pi_workspace_bytes(ctypes.byref(c1)) < lib.pi_workspace_bytes(ctypes.byref(c8))
+    for bad in (3, 32, -1):
+        c = _cfg()
+        c.x_subcells = bad
+        assert lib.pi_workspace_bytes(ctypes.byref(c)) == 0
 
 
 def test_create_rejects_bad_arguments_without_gpu(lib):

@@ -7,6 +7,7 @@ import pytest
 import torch
 
 import synth
+from oracle import celllist
 from oracle import reference as ref
 from tests._util import assert_parity, ctx_for, gpu_interact, oracle_interact, to_dev
 
@@ -177,3 +178,32 @@ def test_c1_sampled(algo):
     # property at full size: sum of forces ~ 0 (antisymmetry), relative to sum |F|
     F = got[:, 1:]
     assert np.all(np.abs(F.sum(0)) <= 1e-4 * np.abs(F).sum(0))
+
+
+@pytest.mark.parametrize("xs", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate"])
+def test_x_subcells(xs, kernel):
+    """Binning order with X sub-cells (R18): per-cell counts/offsets unchanged (bit-exact), and the
+    X-pencil's pruning of sub-cells farther than r_c along X changes no result."""
+    c = synth.scaled_uniform(8, (20, 6, 5), seed=7)
+    want = oracle_interact(c, kernel)
+    ctx = ctx_for(c, kernel, x_subcells=xs)
+    for algo in ALGOS:
+        got, _ = gpu_interact(c, algo, kernel, ctx=ctx)
+        assert_parity(got, want, label=f"x_subcells={xs} {kernel} {algo}")
+    counts, offsets = (t.cpu().numpy() for t in ctx.get_offsets())
+    wc, wo, _ = celllist.binning(celllist.cells(c.x, c.y, c.z, c.grid), c.grid.ncells)
+    assert np.array_equal(counts, wc) and np.array_equal(offsets, wo)
+    assert ctx.stats()["max_per_cell"] == int(wc.max())
+
+
+@pytest.mark.parametrize("nx", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator"])
+def test_narrow_x(nx, kernel):
+    """Grids of 1-5 cells along X: below 4 cells the X-pencil masks the out-of-run halves of a
+    run's end pairs (their partner records can then be within r_c across a row end)."""
+    c = synth.scaled_uniform(8, (nx, 7, 6), seed=11 + nx)
+    want = oracle_interact(c, kernel)
+    for algo in ALGOS:
+        got, _ = gpu_interact(c, algo, kernel)
+        assert_parity(got, want, label=f"nx={nx} {kernel} {algo}")
