@@ -73,8 +73,13 @@ typedef enum {
  *                   phi_i = sum_j q_j K(r_ij),  F_i = (q_i / sigma^2) sum_j q_j K(r_ij) (x_i - x_j)
  *                   (F_i = -grad_i of q_i sum_j q_j K).
  *   PI_K_INDICATOR: phi_i = sum_{j: r_ij < r_c} q_j, F = 0        (test kernel: exact counts)
- *   PI_K_CANDIDATE: phi_i = sum_{j in 27 cells, j != i} q_j, F = 0 (test kernel: no cutoff)    */
-typedef enum { PI_K_GAUSSIAN = 0, PI_K_INDICATOR = 1, PI_K_CANDIDATE = 2 } pi_kernel;
+ *   PI_K_CANDIDATE: phi_i = sum_{j in 27 cells, j != i} q_j, F = 0 (test kernel: no cutoff)
+ *   PI_K_LJ       : the paper's measured kernel, Eq. (1) as printed with the
+ *                   softening of :582 (reading R19): d~ = sqrt(r_ij^2 + eps^2), u = d~ / r,
+ *                   K = 4 E0 (u^12 - u^6); phi_i = sum_j q_j K, F_i = -grad_i (q_i sum_j q_j K);
+ *                   the cutoff test uses the unsoftened r_ij.  kparam[0] = r (0 -> r_c),
+ *                   kparam[1] = eps (>= 0), kparam[2] = E0 (0 -> 1).                          */
+typedef enum { PI_K_GAUSSIAN = 0, PI_K_INDICATOR = 1, PI_K_CANDIDATE = 2, PI_K_LJ = 3 } pi_kernel;
 
 /* Interaction strategy (a6).
  *   PI_A_GLOBAL  : Par-Part-NoLoop (Alg. 1, §4.1): one thread per target,
@@ -96,7 +101,8 @@ typedef struct {
   int32_t dims[3];           /* each >= 1; dims[0] divisible by nranks                      */
   float r_c;                 /* cutoff radius, > 0                                           */
   int32_t kernel;            /* pi_kernel                                                    */
-  float kparam[4];           /* kernel parameters; Gaussian: kparam[0] = sigma (0 -> r_c/3)  */
+  float kparam[4];           /* kernel parameters: Gaussian kparam[0] = sigma (0 -> r_c/3);
+                                LJ kparam[0..2] = r, eps, E0 (see pi_kernel)                  */
   int64_t capacity;          /* max particles resident on this rank (owned + ghosts)        */
   void *stream;              /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)  */
   int32_t rank, nranks;      /* X-slab decomposition (north star); nranks >= 1               */

@@ -73,7 +73,7 @@ int oracle_bin(int64_t n, const int64_t *cell, int64_t ncells, int64_t *counts, 
 }
 
 int oracle_interact(int64_t n, const float *x, const float *y, const float *z, const float *q, const float o[3],
-                    float inv_w, const int32_t d[3], double rc, double sigma, int kernel, double band,
+                    float inv_w, const int32_t d[3], double rc, const double kp[4], int kernel, double band,
                     int64_t nt, const int64_t *targets, double *out, double *S, double *A, int64_t *C,
                     int64_t *P) {
   int64_t ncells = (int64_t)d[0] * d[1] * d[2];
@@ -84,6 +84,8 @@ int oracle_interact(int64_t n, const float *x, const float *y, const float *z, c
   if (!cell || !counts || !offsets || !order) return 1;
   oracle_cells(n, x, y, z, o, inv_w, d, cell);
   oracle_bin(n, cell, ncells, counts, offsets, order);
+  /* kp: Gaussian sigma; Lennard-Jones r, eps, E0 (Eq. (1), reading R19) */
+  const double sigma = kp[0], ljr = kp[1], ljeps = kp[2], lje0 = kp[3];
   const double rc2 = rc * rc, s2 = sigma * sigma, inv2s2 = 1.0 / (2.0 * sigma * sigma);
   if (nt < 0) nt = n;
 #pragma omp parallel for schedule(dynamic, 256)
@@ -116,6 +118,18 @@ int oracle_interact(int64_t n, const float *x, const float *y, const float *z, c
               cij[1] = qi * w * ddx / s2;
               cij[2] = qi * w * ddy / s2;
               cij[3] = qi * w * ddz / s2;
+            } else if (kernel == 3) {
+              /* d~^2 = d^2 + eps^2, s = (d~ / r)^2: K = 4 E0 (s^6 - s^3),
+                 force on i = -q_i q_j dK/dd~ (x_i - x_j) / d~ = q_i q_j G (x_i - x_j) */
+              double s = (r2 + ljeps * ljeps) / (ljr * ljr);
+              double s3 = s * s * s;
+              double K = 4.0 * lje0 * (s3 * s3 - s3);
+              double G = -(4.0 * lje0 / (ljr * ljr)) * (12.0 * s3 * s * s - 6.0 * s * s);
+              double w = (double)q[j];
+              cij[0] = w * K;
+              cij[1] = qi * w * G * ddx;
+              cij[2] = qi * w * G * ddy;
+              cij[3] = qi * w * G * ddz;
             } else {
               cij[0] = (double)q[j];
               cij[1] = cij[2] = cij[3] = 0.0;

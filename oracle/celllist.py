@@ -39,7 +39,7 @@ def _load():
         _lib.oracle_cells.argtypes = [ctypes.c_int64, P, P, P, P, ctypes.c_float, P, P]
         _lib.oracle_bin.argtypes = [ctypes.c_int64, P, ctypes.c_int64, P, P, P]
         _lib.oracle_interact.argtypes = [ctypes.c_int64, P, P, P, P, P, ctypes.c_float, P, ctypes.c_double,
-                                         ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_int64, P,
+                                         P, ctypes.c_int, ctypes.c_double, ctypes.c_int64, P,
                                          P, P, P, P, P]
     return _lib
 
@@ -97,7 +97,7 @@ def interact(x, y, z, q, grid, kernel=ref.KERNEL_GAUSSIAN, targets=None, band=No
     P = np.empty(nt, np.int64)
     if threads is not None:
         set_threads(threads)
+    kp = np.array([float(np.float32(grid.sig)), *ref.lj_params(grid)], dtype=np.float64)
     lib.oracle_interact(len(x), _p(x), _p(y), _p(z), _p(q), _p(o), inv_w, _p(d), float(np.float32(grid.r_c)),
-                        float(np.float32(grid.sig)), int(kernel), float(band), nt, tp, _p(out), _p(S), _p(A),
-                        _p(C), _p(P))
+                        _p(kp), int(kernel), float(band), nt, tp, _p(out), _p(S), _p(A), _p(C), _p(P))
     return dict(out=out, S=S, A=A, C=C, P=P)

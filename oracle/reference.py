@@ -23,6 +23,23 @@ import numpy as np
 KERNEL_GAUSSIAN = 0
 KERNEL_INDICATOR = 1
 KERNEL_CANDIDATE = 2
+KERNEL_LJ = 3
+
+
+def lj_params(grid):
+    """(r, eps, E0) of the Lennard-Jones kernel, rounded to fp32 like every GPU input."""
+    return (float(np.float32(grid.lj_ref)), float(np.float32(grid.lj_soft)), float(np.float32(grid.lj_e0)))
+
+
+def lj_terms(r2, r, eps, e0):
+    """Eq. (1) (§7.1) as printed, with the softening of PAPER.md:582 (reading
+    R19): d~ = sqrt(d^2 + eps^2), u = d~ / r, K = 4 E0 (u^12 - u^6).  Returns K and
+    G = -(dK/dd~) / d~ = -(4 E0 / r^2) (12 u^10 - 6 u^4), so that the force on i from j is
+    q_i q_j G (x_i - x_j) = -grad_i (q_i q_j K)."""
+    s = (r2 + eps * eps) / (r * r)  # u^2
+    K = 4.0 * e0 * (s ** 6 - s ** 3)
+    G = -(4.0 * e0 / (r * r)) * (12.0 * s ** 5 - 6.0 * s ** 2)
+    return K, G
 
 # Ambiguity band for the cutoff decision (DESIGN.md reading R-band): pairs with
 # |r^2 - r_c^2| <= BAND_REL * (w/r_c)^2 * r_c^2 may be included or excluded by an
@@ -137,6 +154,7 @@ def candidate_mask(cc_i, cc_j):
 #   Gaussian  (PAPER.md:52 names the Gaussian; definition = reading Q8 / C8):
 #     K(r) = exp(-r^2 / (2 sigma^2));  c_ij = (q_j K, q_i q_j K (x_i - x_j)/sigma^2, ...)
 #     phi_i = sum_j c_ij[0],  F_i = sum_j c_ij[1:4]   (F_i = -grad_i sum_j q_i q_j K)
+#   LJ:        c_ij = (q_j K, q_i q_j G (x_i - x_j)), K, G of lj_terms (Eq. (1), reading R19)
 #   INDICATOR: c_ij = (q_j, 0, 0, 0) inside the cutoff (test kernel)
 #   CANDIDATE: c_ij = (q_j, 0, 0, 0) for every candidate pair, no cutoff (test kernel)
 # Returned alongside: S_i = sum |c_ij| over included pairs (per component),
@@ -175,6 +193,12 @@ def brute_force(x, y, z, q, grid, kernel=KERNEL_GAUSSIAN, band=None, chunk=512):
             K = np.exp(-r2 * inv2s2)
             c0 = Q[None, :] * K
             cf = (Q[s:e, None] * Q[None, :] * K / (sig * sig))[:, :, None] * d
+            comps = np.concatenate([c0[:, :, None], cf], axis=2)
+            incl = inside
+        elif kernel == KERNEL_LJ:
+            K, G = lj_terms(r2, *lj_params(grid))
+            c0 = Q[None, :] * K
+            cf = (Q[s:e, None] * Q[None, :] * G)[:, :, None] * d
             comps = np.concatenate([c0[:, :, None], cf], axis=2)
             incl = inside
         elif kernel == KERNEL_INDICATOR:

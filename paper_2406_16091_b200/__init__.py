@@ -29,7 +29,7 @@ class PiError(RuntimeError):
 
 
 def _config(dims, cell_width, r_c=None, origin=(0.0, 0.0, 0.0), kernel="gaussian", sigma=0.0, capacity=0,
-            rank=0, nranks=1, x_subcells=0):
+            rank=0, nranks=1, x_subcells=0, lj=(0.0, 0.0, 0.0)):
     cfg = L.pi_config()
     for a in range(3):
         cfg.origin[a] = float(origin[a])
@@ -37,7 +37,11 @@ def _config(dims, cell_width, r_c=None, origin=(0.0, 0.0, 0.0), kernel="gaussian
     cfg.cell_width = float(cell_width)
     cfg.r_c = float(cell_width if r_c is None else r_c)
     cfg.kernel = L.KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
-    cfg.kparam[0] = float(sigma)
+    if cfg.kernel == L.KERNELS["lj"]:  # Lennard-Jones r, eps, E0 (0 -> r_c, 0, 1)
+        for k in range(3):
+            cfg.kparam[k] = float(lj[k])
+    else:
+        cfg.kparam[0] = float(sigma)
     cfg.capacity = int(capacity)
     cfg.rank = int(rank)
     cfg.nranks = int(nranks)
@@ -79,12 +83,14 @@ class Context:
     """One libpi context on one GPU (pi_create / pi_destroy).
 
     dims, cell_width, origin: the cell grid (cell_width >= r_c, PAPER.md:93);
-    kernel: 'gaussian' | 'indicator' | 'candidate'; sigma: Gaussian width (0 -> r_c/3);
+    kernel: 'gaussian' | 'indicator' | 'candidate' | 'lj'; sigma: Gaussian width (0 -> r_c/3);
+    lj: Lennard-Jones (r, eps, E0) of Eq. (1) (0 -> r_c, 0, 1);
     capacity: max particles resident.
     """
 
     def __init__(self, dims, cell_width, r_c=None, origin=(0.0, 0.0, 0.0), kernel="gaussian", sigma=0.0,
-                 capacity=0, device=None, stream=None, rank=0, nranks=1, nccl_unique_id=None, x_subcells=0):
+                 capacity=0, device=None, stream=None, rank=0, nranks=1, nccl_unique_id=None, x_subcells=0,
+                 lj=(0.0, 0.0, 0.0)):
         self._lib = L.load()
         self.device = torch.device(device if device is not None else "cuda")
         self.dims = tuple(int(d) for d in dims)
@@ -92,7 +98,7 @@ class Context:
         self.r_c = float(cell_width if r_c is None else r_c)
         self.origin = tuple(float(o) for o in origin)
         cfg = _config(self.dims, self.cell_width, self.r_c, self.origin, kernel, sigma, capacity, rank, nranks,
-                      x_subcells)
+                      x_subcells, lj)
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         self.stream = stream

@@ -196,7 +196,11 @@ static bool config_ok(const pi_config *cfg, char *why, size_t n) {
   if (!(cfg->cell_width > 0.f)) { snprintf(why, n, "cell_width must be > 0"); return false; }
   if (!(cfg->r_c > 0.f)) { snprintf(why, n, "r_c must be > 0"); return false; }
   if (cfg->r_c > cfg->cell_width) { snprintf(why, n, "cell_width must be >= r_c (PAPER.md:93)"); return false; }
-  if (cfg->kernel < 0 || cfg->kernel > 2) { snprintf(why, n, "unknown kernel"); return false; }
+  if (cfg->kernel < 0 || cfg->kernel > 3) { snprintf(why, n, "unknown kernel"); return false; }
+  if (cfg->kernel == PI_K_LJ && (cfg->kparam[0] < 0.f || cfg->kparam[1] < 0.f)) {
+    snprintf(why, n, "Lennard-Jones r and eps must be >= 0");
+    return false;
+  }
   if (cfg->capacity < 0 || cfg->capacity > (1LL << 31) - 64) { snprintf(why, n, "capacity out of range"); return false; }
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) { snprintf(why, n, "bad rank/nranks"); return false; }
   if (cfg->dims[0] % cfg->nranks) { snprintf(why, n, "dims[0] must be divisible by nranks"); return false; }
@@ -290,12 +294,23 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   k.kernel = cfg->kernel;
   k.rc = cfg->r_c;
   k.rc2 = cfg->r_c * cfg->r_c;
-  float sigma = cfg->kparam[0] > 0.f ? cfg->kparam[0] : cfg->r_c / 3.0f;
+  float sigma = (cfg->kernel == PI_K_GAUSSIAN && cfg->kparam[0] > 0.f) ? cfg->kparam[0] : cfg->r_c / 3.0f;
   k.sigma = sigma;
   k.inv_s2 = (float)(1.0 / ((double)sigma * (double)sigma));
   k.c2 = (float)(1.4426950408889634 / (2.0 * (double)sigma * (double)sigma));
   k.s = (float)std::sqrt((double)k.c2);
   k.s_inv = (float)(1.0 / std::sqrt((double)k.c2));
+  k.phi_scale = 1.0f;
+  k.f_ts = k.inv_s2;
+  if (cfg->kernel == PI_K_LJ) {  // Eq. (1), reading R19
+    const double r = cfg->kparam[0] > 0.f ? cfg->kparam[0] : cfg->r_c;
+    const double eps = cfg->kparam[1];
+    const double e0 = cfg->kparam[2] > 0.f ? cfg->kparam[2] : 1.0;
+    k.lj_inv_r2 = (float)(1.0 / (r * r));
+    k.lj_e2 = (float)(eps * eps / (r * r));
+    k.phi_scale = (float)(4.0 * e0);
+    k.f_ts = (float)(-4.0 * e0 / (r * r));
+  }
   // zero the control block, counts (the scan keeps them zero afterwards) and scan status
   cudaError_t e = cudaMemsetAsync(c->ws, 0, lay.rec, c->stream);
   if (e != cudaSuccess) {

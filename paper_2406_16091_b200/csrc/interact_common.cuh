@@ -54,6 +54,30 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
       "r"(parity)
       : "memory");
 }
+// Wait with backoff, for a warp that has nothing else to do (a producer waiting for its slot
+// to be released): without the sleep its try_wait loop takes issue slots from the compute
+// warps of its scheduler for the whole wait.
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long *bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long *bar, unsigned parity) {
+  unsigned ns = 64;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 2048 ? 2 * ns : 2048;
+  }
+}
+
 // 1-D bulk copy global -> shared (TMA, SASS UBLKCP); dst/src 16-B aligned, bytes % 16 == 0.
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
   asm volatile(
@@ -87,11 +111,31 @@ __device__ __forceinline__ SrcPair load_pair(const float4 *__restrict__ S, int p
   return r;
 }
 
+// Lennard-Jones core (Eq. (1), reading R19) on f32x2 values: s = (d~/r)^2 = r2 / r^2 + eps^2 / r^2;
+// returns the potential and force weights of the pair halves with q masked to the cutoff
+// (qm = r2 < r_c^2 ? q : 0):  w = qm (s^6 - s^3),  wf = qm (12 s^5 - 6 s^2).
+__device__ __forceinline__ void lj_core(p2 r2, p2 q, const float thr, const KParams &kp, p2 &w, p2 &wf) {
+  // clamp to r_c^2 before the powers: an inert padding partner (x = 1e30) would give s = inf,
+  // inf - inf = NaN and NaN * 0 = NaN; masked halves only need finite values
+  const p2 rc = pk(fminf(lo(r2), thr), fminf(hi(r2), thr));
+  const p2 s = fma2(rc, pk(kp.lj_inv_r2), pk(kp.lj_e2));
+  const p2 s2 = mul2(s, s);
+  const p2 s3 = mul2(s2, s);
+  const p2 s6 = mul2(s3, s3);
+  const p2 s5 = mul2(s3, s2);
+  const p2 pot = add2(s6, pk(-lo(s3), -hi(s3)));
+  const p2 fk = fma2(s5, pk(12.f), mul2(s2, pk(-6.f)));
+  const p2 qm = pk((lo(r2) < thr) ? lo(q) : 0.f, (hi(r2) < thr) ? hi(q) : 0.f);
+  w = mul2(pot, qm);
+  wf = mul2(fk, qm);
+}
+
 // One source pair against the thread's target (xt, yt, zt); thr = r_c^2, mc2 = -c2.
-// 12 packed-fp32 operations and 2 MUFU.EX2 for 2 candidates.
+// Gaussian: 12 packed-fp32 operations and 2 MUFU.EX2 for 2 candidates.
 template <int KERNEL>
 __device__ __forceinline__ void src_eval(const SrcPair &s, float xt, float yt, float zt, const float thr,
-                                         const float mc2, p2 &phi, p2 &fx, p2 &fy, p2 &fz) {
+                                         const float mc2, p2 &phi, p2 &fx, p2 &fy, p2 &fz,
+                                         const KParams *kp = nullptr) {
   if (KERNEL == PI_K_CANDIDATE) {
     phi = add2(phi, s.q);
     return;
@@ -112,6 +156,13 @@ __device__ __forceinline__ void src_eval(const SrcPair &s, float xt, float yt, f
     fx = fma2(w, dx, fx);
     fy = fma2(w, dy, fy);
     fz = fma2(w, dz, fz);
+  } else if (KERNEL == PI_K_LJ) {
+    p2 w, wf;
+    lj_core(r2, s.q, thr, *kp, w, wf);
+    phi = add2(phi, w);
+    fx = fma2(wf, dx, fx);
+    fy = fma2(wf, dy, fy);
+    fz = fma2(wf, dz, fz);
   } else {
     const float k0 = (lo(r2) < thr) ? lo(s.q) : 0.f;
     const float k1 = (hi(r2) < thr) ? hi(s.q) : 0.f;
@@ -119,101 +170,30 @@ __device__ __forceinline__ void src_eval(const SrcPair &s, float xt, float yt, f
   }
 }
 
-// The exact rounded phi term the lane added for source half h of pair s against its own
-// target.  For the self pair d = 0 exactly, so it added nothing to F.
+// The phi term a walk over the self pair adds for a target of value q (d = 0): q for the
+// Gaussian (K(0) = 2^0 = 1), INDICATOR and CANDIDATE kernels; for LJ the same rounded
+// operations as lj_core at r2 = 0 (fma(0, ., e2) = e2), so the subtraction is exact.
 template <int KERNEL>
-__device__ __forceinline__ float self_phi(const SrcPair &s, int h, float xt, float yt, float zt, const float thr,
-                                          const float mc2) {
-  if (KERNEL == PI_K_CANDIDATE) return h ? hi(s.q) : lo(s.q);
-  const p2 dx = add2(s.x, pk(-xt));
-  const p2 dy = add2(s.y, pk(-yt));
-  const p2 dz = add2(s.z, pk(-zt));
-  p2 r2 = mul2(dx, dx);
-  r2 = fma2(dy, dy, r2);
-  r2 = fma2(dz, dz, r2);
-  const p2 arg = mul2(r2, pk(mc2));
-  const float rr = h ? hi(r2) : lo(r2);
-  const float ar = h ? hi(arg) : lo(arg);
-  const float q = h ? hi(s.q) : lo(s.q);
-  if (KERNEL == PI_K_GAUSSIAN) return (rr < thr) ? __fmul_rn(ex2_approx(ar), q) : 0.f;
-  return (rr < thr) ? q : 0.f;
+__device__ __forceinline__ float self_term(float q, const KParams &kp) {
+  if (KERNEL != PI_K_LJ) return q;
+  const float s = kp.lj_e2;
+  const float s2 = __fmul_rn(s, s), s3 = __fmul_rn(s2, s), s6 = __fmul_rn(s3, s3);
+  return __fmul_rn(__fsub_rn(s6, s3), q);
 }
 
-// Staging transform, in place on a pair of raw (x, y, z, q) records -> the pair layout above
-// (a pure interleave: the values are the bitwise fp32 inputs).
-__device__ __forceinline__ void stage_pair(float4 *S, int p) {
-  const float4 a = S[2 * p], b = S[2 * p + 1];
-  S[2 * p] = make_float4(a.x, b.x, a.y, b.y);
-  S[2 * p + 1] = make_float4(a.z, b.z, a.w, b.w);
-}
-
-// One thread, one target (pair index pt, half ht) against source pairs [p0, p1) of S.
-// Returns (phi, sum w d) summed over both halves, self pair removed; F = -(q_t/sigma^2) sum w d.
-template <int KERNEL, int UNR = 4>
-__device__ __forceinline__ float4 lane_target(const float4 *__restrict__ S, int pt, int ht, int p0, int p1,
-                                              const float thr, const float mc2) {
-  float xt, yt, zt;
-  {
-    const float4 a = S[2 * pt], b = S[2 * pt + 1];
-    xt = ht ? a.y : a.x;
-    yt = ht ? a.w : a.z;
-    zt = ht ? b.y : b.x;
-  }
-  p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
-  int p = p0;
-  // 4 source pairs per iteration into two independent accumulator sets (ILP), or 2 pairs
-  // into one set when registers are the occupancy limit
-  p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
-  if (UNR == 2) {
-    for (; p + 2 <= p1; p += 2) {
-      const SrcPair s0 = load_pair(S, p), s1 = load_pair(S, p + 1);
-      src_eval<KERNEL>(s0, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
-      src_eval<KERNEL>(s1, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
-    }
-  }
-  for (; UNR == 4 && p + 4 <= p1; p += 4) {
-    const SrcPair s0 = load_pair(S, p), s1 = load_pair(S, p + 1), s2 = load_pair(S, p + 2),
-                  s3 = load_pair(S, p + 3);
-    src_eval<KERNEL>(s0, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
-    src_eval<KERNEL>(s1, xt, yt, zt, thr, mc2, phb, fxb, fyb, fzb);
-    src_eval<KERNEL>(s2, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
-    src_eval<KERNEL>(s3, xt, yt, zt, thr, mc2, phb, fxb, fyb, fzb);
-  }
-  for (; p < p1; ++p) src_eval<KERNEL>(load_pair(S, p), xt, yt, zt, thr, mc2, phi, fx, fy, fz);
-  phi = add2(phi, phb);
-  fx = add2(fx, fxb);
-  fy = add2(fy, fyb);
-  fz = add2(fz, fzb);
-  // identity exclusion (Alg. 1 :127)
-  const float self = self_phi<KERNEL>(load_pair(S, pt), ht, xt, yt, zt, thr, mc2);
-  if (ht) phi = pk(lo(phi), hi(phi) - self);
-  else phi = pk(lo(phi) - self, hi(phi));
-  return make_float4(lo(phi) + hi(phi), lo(fx) + hi(fx), lo(fy) + hi(fy), lo(fz) + hi(fz));
-}
-
-// One lane's share of one target's window: source pairs p = pb, pb + st, pb + 2 st, ... < pe
-// (st lanes share the target).  Returns (phi, sum w d) over both halves, self pair INCLUDED
-// (the caller subtracts self_phi once after combining the lanes).
+// Scalar contribution of a source of value qs at squared distance r2 (inside the cutoff):
+// w (phi, before phi_scale) and wf (force weight: F += wf (x_t - x_s), before q_t f_ts).
 template <int KERNEL>
-__device__ __forceinline__ float4 lane_window(const float4 *__restrict__ S, float xt, float yt, float zt, int pb,
-                                              int pe, int st, const float thr, const float mc2) {
-  p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
-  p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
-  int p = pb;
-  for (; p + 3 * st < pe; p += 4 * st) {
-    const SrcPair s0 = load_pair(S, p), s1 = load_pair(S, p + st), s2 = load_pair(S, p + 2 * st),
-                  s3 = load_pair(S, p + 3 * st);
-    src_eval<KERNEL>(s0, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
-    src_eval<KERNEL>(s1, xt, yt, zt, thr, mc2, phb, fxb, fyb, fzb);
-    src_eval<KERNEL>(s2, xt, yt, zt, thr, mc2, phi, fx, fy, fz);
-    src_eval<KERNEL>(s3, xt, yt, zt, thr, mc2, phb, fxb, fyb, fzb);
+__device__ __forceinline__ void scalar_term(const KParams &kp, float r2, float qs, float &w, float &wf) {
+  if (KERNEL == PI_K_LJ) {
+    const float s = fmaf(r2, kp.lj_inv_r2, kp.lj_e2);
+    const float s2 = s * s, s3 = s2 * s, s6 = s3 * s3, s5 = s3 * s2;
+    w = (s6 - s3) * qs;
+    wf = fmaf(s5, 12.f, s2 * -6.f) * qs;
+  } else {
+    w = qs * ex2_approx(-kp.c2 * r2);
+    wf = w;
   }
-  for (; p < pe; p += st) src_eval<KERNEL>(load_pair(S, p), xt, yt, zt, thr, mc2, phi, fx, fy, fz);
-  phi = add2(phi, phb);
-  fx = add2(fx, fxb);
-  fy = add2(fy, fyb);
-  fz = add2(fz, fzb);
-  return make_float4(lo(phi) + hi(phi), lo(fx) + hi(fx), lo(fy) + hi(fy), lo(fz) + hi(fz));
 }
 
 // Fallback for a target whose cell window does not fit the staging buffer: Par-Part-NoLoop
@@ -245,19 +225,21 @@ __device__ void fallback_target(int t, int cx, int cy, int cz, const float4 *__r
           if (KERNEL == PI_K_INDICATOR) {
             phi += o.w;
           } else {
-            const float w = o.w * ex2_approx(-kp.c2 * r2);
+            float w, wf;
+            scalar_term<KERNEL>(kp, r2, o.w, w, wf);
             phi += w;
-            fx = fmaf(w, dx, fx);
-            fy = fmaf(w, dy2, fy);
-            fz = fmaf(w, dz2, fz);
+            fx = fmaf(wf, dx, fx);
+            fy = fmaf(wf, dy2, fy);
+            fz = fmaf(wf, dz2, fz);
           }
         }
       }
     }
   }
   cand -= 1;
-  if (KERNEL == PI_K_GAUSSIAN) {
-    const float sc = me.w * kp.inv_s2;
+  if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+    const float sc = me.w * kp.f_ts;
+    phi *= kp.phi_scale;
     fx *= sc; fy *= sc; fz *= sc;
   } else {
     fx = fy = fz = 0.f;

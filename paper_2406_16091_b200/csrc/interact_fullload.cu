@@ -53,7 +53,7 @@ struct TgtPair {
 // One source (scalar broadcast) against the thread's two targets: 12 packed ops, 2 MUFU.
 template <int KERNEL>
 __device__ __forceinline__ void tp_eval(const TgtPair &t, const float4 a, const float thr, const float mc2, p2 &phi,
-                                        p2 &fx, p2 &fy, p2 &fz) {
+                                        p2 &fx, p2 &fy, p2 &fz, const KParams &kp) {
   if (KERNEL == PI_K_CANDIDATE) {
     phi = add2(phi, pk(a.w));
     return;
@@ -73,6 +73,13 @@ __device__ __forceinline__ void tp_eval(const TgtPair &t, const float4 a, const 
     fx = fma2(w, dx, fx);
     fy = fma2(w, dy, fy);
     fz = fma2(w, dz, fz);
+  } else if (KERNEL == PI_K_LJ) {
+    p2 w, wf;
+    lj_core(r2, pk(a.w), thr, kp, w, wf);
+    phi = add2(phi, w);
+    fx = fma2(wf, dx, fx);
+    fy = fma2(wf, dy, fy);
+    fz = fma2(wf, dz, fz);
   } else {
     phi = add2(phi, pk((lo(r2) < thr) ? a.w : 0.f, (hi(r2) < thr) ? a.w : 0.f));
   }
@@ -80,8 +87,20 @@ __device__ __forceinline__ void tp_eval(const TgtPair &t, const float4 a, const 
 
 // The exact phi term added for target half h against itself (d = 0: no force term).
 template <int KERNEL>
-__device__ __forceinline__ float tp_self(const TgtPair &t, int h, const float4 a, const float thr, const float mc2) {
+__device__ __forceinline__ float tp_self(const TgtPair &t, int h, const float4 a, const float thr, const float mc2,
+                                         const KParams &kp) {
   if (KERNEL == PI_K_CANDIDATE) return a.w;
+  if (KERNEL == PI_K_LJ) {  // the same lj_core operations as tp_eval, this half
+    const p2 dx = add2(t.x, pk(-a.x));
+    const p2 dy = add2(t.y, pk(-a.y));
+    const p2 dz = add2(t.z, pk(-a.z));
+    p2 r2 = mul2(dx, dx);
+    r2 = fma2(dy, dy, r2);
+    r2 = fma2(dz, dz, r2);
+    p2 w, wf;
+    lj_core(r2, pk(a.w), thr, kp, w, wf);
+    return h ? hi(w) : lo(w);
+  }
   const p2 dx = add2(t.x, pk(-a.x));
   const p2 dy = add2(t.y, pk(-a.y));
   const p2 dz = add2(t.z, pk(-a.z));
@@ -221,28 +240,28 @@ __global__ void __launch_bounds__(NT) k_interact_fullload(FlParams p) {
         int s = s0;
         for (; s + 2 <= s1; s += 2) {
           const float4 u = S[s], v = S[s + 1];
-          tp_eval<KERNEL>(tp, u, thr, mc2, phi, fx, fy, fz);
-          tp_eval<KERNEL>(tp, v, thr, mc2, phi, fx, fy, fz);
+          tp_eval<KERNEL>(tp, u, thr, mc2, phi, fx, fy, fz, p.kp);
+          tp_eval<KERNEL>(tp, v, thr, mc2, phi, fx, fy, fz, p.kp);
         }
-        if (s < s1) tp_eval<KERNEL>(tp, S[s], thr, mc2, phi, fx, fy, fz);
+        if (s < s1) tp_eval<KERNEL>(tp, S[s], thr, mc2, phi, fx, fy, fz, p.kp);
       }
       // identity exclusion (Alg. 1 :127)
-      phi = pk(lo(phi) - tp_self<KERNEL>(tp, 0, a0, thr, mc2), hi(phi));
-      if (t1 != t0) phi = pk(lo(phi), hi(phi) - tp_self<KERNEL>(tp, 1, a1, thr, mc2));
+      phi = pk(lo(phi) - tp_self<KERNEL>(tp, 0, a0, thr, mc2, p.kp), hi(phi));
+      if (t1 != t0) phi = pk(lo(phi), hi(phi) - tp_self<KERNEL>(tp, 1, a1, thr, mc2, p.kp));
       cand += (unsigned long long)(t1 - t0 + 1) * (unsigned long long)(ncand - 1);
       const int gs0 = O[rh * BX3 + cx + 1] + 2 * i;
       const float4 me0 = p.out.upd ? __ldg(p.rec + gs0) : a0;
-      if (KERNEL == PI_K_GAUSSIAN) {
-        const float c0 = a0.w * p.kp.inv_s2;
-        write_output(p.out, g, gs0, me0, lo(phi), c0 * lo(fx), c0 * lo(fy), c0 * lo(fz));
+      if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+        const float c0 = a0.w * p.kp.f_ts;  // summed wf (x_t - x_s)
+        write_output(p.out, g, gs0, me0, lo(phi) * p.kp.phi_scale, c0 * lo(fx), c0 * lo(fy), c0 * lo(fz));
       } else {
         write_output(p.out, g, gs0, me0, lo(phi), 0.f, 0.f, 0.f);
       }
       if (t1 != t0) {
         const float4 me1 = p.out.upd ? __ldg(p.rec + gs0 + 1) : a1;
-        if (KERNEL == PI_K_GAUSSIAN) {
-          const float c1 = a1.w * p.kp.inv_s2;
-          write_output(p.out, g, gs0 + 1, me1, hi(phi), c1 * hi(fx), c1 * hi(fy), c1 * hi(fz));
+        if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+          const float c1 = a1.w * p.kp.f_ts;
+          write_output(p.out, g, gs0 + 1, me1, hi(phi) * p.kp.phi_scale, c1 * hi(fx), c1 * hi(fy), c1 * hi(fz));
         } else {
           write_output(p.out, g, gs0 + 1, me1, hi(phi), 0.f, 0.f, 0.f);
         }
@@ -272,6 +291,7 @@ cudaError_t launch_nt(const FlParams &p, cudaStream_t s) {
   switch (p.kp.kernel) {
     case PI_K_GAUSSIAN: return launch_k<PI_K_GAUSSIAN, NT>(p, s);
     case PI_K_INDICATOR: return launch_k<PI_K_INDICATOR, NT>(p, s);
+    case PI_K_LJ: return launch_k<PI_K_LJ, NT>(p, s);
     default: return launch_k<PI_K_CANDIDATE, NT>(p, s);
   }
 }

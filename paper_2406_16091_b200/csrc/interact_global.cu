@@ -8,7 +8,7 @@
 // source is one LDG.128; the 3 cells of a neighbour row (dx = -1..1) are contiguous in the
 // X-fastest order, so the 27 cells are walked as 9 contiguous runs.
 // r^2 is computed directly (dx^2 + dy^2 + dz^2) and the cutoff test is strict (<).
-#include "pi_internal.cuh"
+#include "interact_common.cuh"
 
 namespace pi {
 namespace {
@@ -59,19 +59,21 @@ __global__ void __launch_bounds__(PPNL_THREADS) k_interact_global(long long n, c
             if (KERNEL == PI_K_INDICATOR) {
               phi += o.w;
             } else {
-              const float w = o.w * ex2_approx(-kp.c2 * r2);
+              float w, wf;
+              scalar_term<KERNEL>(kp, r2, o.w, w, wf);
               phi += w;
-              fx = fmaf(w, dx, fx);
-              fy = fmaf(w, dy2, fy);
-              fz = fmaf(w, dz2, fz);
+              fx = fmaf(wf, dx, fx);
+              fy = fmaf(wf, dy2, fy);
+              fz = fmaf(wf, dz2, fz);
             }
           }
         }
       }
     }
     cand -= 1;  // self
-    if (KERNEL == PI_K_GAUSSIAN) {
-      const float s = me.w * kp.inv_s2;
+    if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+      const float s = me.w * kp.f_ts;  // summed wf (x_t - x_s)
+      phi *= kp.phi_scale;
       fx *= s; fy *= s; fz *= s;
     } else {
       fx = fy = fz = 0.f;
@@ -96,6 +98,9 @@ cudaError_t launch_interact_global(const Geom &g, const KParams &k, const Intera
     case PI_K_INDICATOR:
       k_interact_global<PI_K_INDICATOR><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl,
                                                                          a.n_dev);
+      break;
+    case PI_K_LJ:
+      k_interact_global<PI_K_LJ><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl, a.n_dev);
       break;
     default:
       k_interact_global<PI_K_CANDIDATE><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl,

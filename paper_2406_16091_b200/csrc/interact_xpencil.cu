@@ -176,7 +176,7 @@ __device__ int choose_round(const XpParams &p, const Slot &sl, int ja, int Lseg)
 // The self term (= q_t exactly: d = 0, K(0) = 2^0 = 1) is removed.
 template <int KERNEL, bool MASK>
 __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, int klo, int khi, const float4 me,
-                                        const float thr, const float mc2) {
+                                        const float thr, const float mc2, const KParams &kp) {
   const float4 *__restrict__ S = sl.S;
   p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
   p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
@@ -190,36 +190,38 @@ __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, 
       int q = p0;
       for (; q + 1 <= pl; q += 2) {
         const SrcPair s0 = load_pair(S, q), s1 = load_pair(S, q + 1);
-        src_eval<KERNEL>(s0, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz);
-        src_eval<KERNEL>(s1, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb);
+        src_eval<KERNEL>(s0, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
+        src_eval<KERNEL>(s1, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
       }
-      if (q <= pl) src_eval<KERNEL>(load_pair(S, q), me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz);
+      if (q <= pl) src_eval<KERNEL>(load_pair(S, q), me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
       continue;
     }
     {
       SrcPair f = load_pair(S, p0);
       f.q = pk((a & 1) ? 0.f : lo(f.q), (p0 == pl && (b & 1)) ? 0.f : hi(f.q));
-      src_eval<KERNEL>(f, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz);
+      src_eval<KERNEL>(f, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
     }
     if (pl > p0) {
       int q = p0 + 1;
       for (; q + 2 <= pl; q += 2) {
         const SrcPair s0 = load_pair(S, q), s1 = load_pair(S, q + 1);
-        src_eval<KERNEL>(s0, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb);
-        src_eval<KERNEL>(s1, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz);
+        src_eval<KERNEL>(s0, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
+        src_eval<KERNEL>(s1, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
       }
-      if (q < pl) src_eval<KERNEL>(load_pair(S, q), me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb);
+      if (q < pl) src_eval<KERNEL>(load_pair(S, q), me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
       SrcPair l = load_pair(S, pl);
       l.q = pk(lo(l.q), (b & 1) ? 0.f : hi(l.q));
-      src_eval<KERNEL>(l, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb);
+      src_eval<KERNEL>(l, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
     }
   }
   phi = add2(phi, phb);
   fx = add2(fx, fxb);
   fy = add2(fy, fyb);
   fz = add2(fz, fzb);
-  // identity exclusion (Alg. 1 :127): the self pair added exactly q_t to phi and 0 to F
-  return make_float4(lo(phi) + hi(phi) - me.w, lo(fx) + hi(fx), lo(fy) + hi(fy), lo(fz) + hi(fz));
+  // identity exclusion (Alg. 1 :127): remove the exact term the self pair added to phi
+  // (q_t, or the LJ value at d = 0; it added nothing to F)
+  return make_float4(lo(phi) + hi(phi) - self_term<KERNEL>(me.w, kp), lo(fx) + hi(fx), lo(fy) + hi(fy),
+                     lo(fz) + hi(fz));
 }
 
 template <int KERNEL, int NC>
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       const int s = use % NSLOT;
       const Slot sl = slot_at(slots, L, p.capp, sx, s);
       XP_T(t0);
-      if (use >= NSLOT) mbar_wait(&empty[s], ((use / NSLOT) - 1) & 1);  // consumers released it
+      if (use >= NSLOT) mbar_wait_sleep(&empty[s], ((use / NSLOT) - 1) & 1);  // consumers released it
       XP_T(t1);
       XP_ADD(0, t0, t1);
       fence_proxy_async();  // their generic reads of the slot precede the TMA writes below
@@ -356,15 +358,15 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
             // (the CANDIDATE test kernel counts every candidate: no pruning)
             const int klo = KERNEL == PI_K_CANDIDATE ? (j - 1) * sx : min(max(flo, (j - 1) * sx), (j + 2) * sx - 1);
             const int khi = KERNEL == PI_K_CANDIDATE ? (j + 2) * sx - 1 : min(max(fhi, (j - 1) * sx), (j + 2) * sx - 1);
-            const float4 r = p.mask ? walk9<KERNEL, true>(sl, LF, sx, ja, klo, khi, me, thr, mc2)
-                                    : walk9<KERNEL, false>(sl, LF, sx, ja, klo, khi, me, thr, mc2);
+            const float4 r = p.mask ? walk9<KERNEL, true>(sl, LF, sx, ja, klo, khi, me, thr, mc2, p.kp)
+                                    : walk9<KERNEL, false>(sl, LF, sx, ja, klo, khi, me, thr, mc2, p.kp);
             int nc = 0;  // the 27-cell candidates (the unit of the metric, R4), pruned or not
 #pragma unroll
             for (int rr = 0; rr < 9; ++rr) nc += sl.O[rr * LF + (j + 2) * sx] - sl.O[rr * LF + (j - 1) * sx];
             cand += (unsigned long long)(nc - 1);
-            if (KERNEL == PI_K_GAUSSIAN) {
-              const float sc = -me.w * p.kp.inv_s2;
-              write_output(p.out, g, gs, me, r.x, sc * r.y, sc * r.z, sc * r.w);
+            if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+              const float sc = -me.w * p.kp.f_ts;  // the walk summed wf (x_s - x_t)
+              write_output(p.out, g, gs, me, r.x * p.kp.phi_scale, sc * r.y, sc * r.z, sc * r.w);
             } else {
               write_output(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f);
             }
@@ -411,6 +413,7 @@ cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
   switch (p.kp.kernel) {
     case PI_K_GAUSSIAN: return go(k_interact_xpencil<PI_K_GAUSSIAN, NC>);
     case PI_K_INDICATOR: return go(k_interact_xpencil<PI_K_INDICATOR, NC>);
+    case PI_K_LJ: return go(k_interact_xpencil<PI_K_LJ, NC>);
     default: return go(k_interact_xpencil<PI_K_CANDIDATE, NC>);
   }
 }

@@ -28,7 +28,12 @@ struct KParams {
   float rc, rc2;
   float sigma, inv_s2;  // 1/sigma^2
   float c2;             // log2(e) / (2 sigma^2): K = 2^(-c2 r^2)
-  float s, s_inv;       // sqrt(c2) and 1/sqrt(c2): coordinate scale of the staged kernels
+  float s, s_inv;       // sqrt(c2) and 1/sqrt(c2)
+  float lj_inv_r2, lj_e2;  // Lennard-Jones: 1/r^2 and eps^2/r^2, so (d~/r)^2 = d^2 lj_inv_r2 + lj_e2
+  // Output scales: phi = phi_scale sum w;  F = q_t f_ts sum wf (x_t - x_s), where a source
+  // contributes w = q_s K (Gaussian; K = 2^(-c2 r^2)) or q_s (s^6 - s^3) (LJ), and
+  // wf = w (Gaussian) or q_s (12 s^5 - 6 s^2) (LJ):  Gaussian 1, 1/sigma^2;  LJ 4 E0, -4 E0 / r^2
+  float phi_scale, f_ts;
 };
 
 // Device-resident control / statistics block (in the workspace).

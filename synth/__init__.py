@@ -38,10 +38,21 @@ class Grid:
     origin: tuple = (0.0, 0.0, 0.0)
     rc: float | None = None
     sigma: float | None = None
+    lj_r: float | None = None      # Lennard-Jones reference length r of Eq. (1) (default r_c)
+    lj_eps: float | None = None    # softening (default r_c / 20)
+    lj_e0: float = 1.0             # E_0
 
     @property
     def r_c(self) -> float:
         return float(self.w if self.rc is None else self.rc)
+
+    @property
+    def lj_ref(self) -> float:
+        return float(self.r_c if self.lj_r is None else self.lj_r)
+
+    @property
+    def lj_soft(self) -> float:
+        return float(self.r_c / 20.0 if self.lj_eps is None else self.lj_eps)
 
     @property
     def sig(self) -> float:

@@ -12,6 +12,8 @@ def ctx_for(cloud, kernel="gaussian", capacity=None, **kw):
     from paper_2406_16091_b200 import Context
     g = cloud.grid
     cap = capacity if capacity is not None else max(cloud.n, 1)
+    if kernel == "lj":
+        kw.setdefault("lj", (g.lj_ref, g.lj_soft, g.lj_e0))
     return Context(g.dims, g.w, g.r_c, g.origin, kernel=kernel, sigma=0.0 if g.sigma is None else g.sigma,
                    capacity=cap, device="cuda", **kw)
 
@@ -33,7 +35,8 @@ def gpu_interact(cloud, algo, kernel="gaussian", tuning=None, ctx=None):
     return out, ctx
 
 
-KERNEL_ID = {"gaussian": ref.KERNEL_GAUSSIAN, "indicator": ref.KERNEL_INDICATOR, "candidate": ref.KERNEL_CANDIDATE}
+KERNEL_ID = {"gaussian": ref.KERNEL_GAUSSIAN, "indicator": ref.KERNEL_INDICATOR, "candidate": ref.KERNEL_CANDIDATE,
+             "lj": ref.KERNEL_LJ}
 
 
 def oracle_interact(cloud, kernel="gaussian", targets=None, band=None):

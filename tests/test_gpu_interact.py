@@ -19,14 +19,14 @@ EXACT_BOUNDARY = {"global": True, "xpencil": True, "fullload": True}
 
 
 @pytest.mark.parametrize("algo", ALGOS)
-@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate"])
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate", "lj"])
 def test_c0_full(algo, kernel):
     """configs[0]: 4096 uniform particles, 16^3 cells, every particle vs the oracle."""
     c = synth.make_config("c0")
     got, ctx = gpu_interact(c, algo, kernel)
     want = oracle_interact(c, kernel)
     assert_parity(got, want, label=f"c0 {algo} {kernel}")
-    if kernel != "gaussian":
+    if kernel in ("indicator", "candidate"):
         assert np.all(got[:, 1:] == 0)
     st = ctx.stats()
     assert st["candidates"] == int(want["C"].sum())
@@ -181,7 +181,7 @@ def test_c1_sampled(algo):
 
 
 @pytest.mark.parametrize("xs", [1, 2, 4, 8, 16])
-@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate"])
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate", "lj"])
 def test_x_subcells(xs, kernel):
     """Binning order with X sub-cells (R18): per-cell counts/offsets unchanged (bit-exact), and the
     X-pencil's pruning of sub-cells farther than r_c along X changes no result."""
@@ -198,7 +198,7 @@ def test_x_subcells(xs, kernel):
 
 
 @pytest.mark.parametrize("nx", [1, 2, 3, 4, 5])
-@pytest.mark.parametrize("kernel", ["gaussian", "indicator"])
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "lj"])
 def test_narrow_x(nx, kernel):
     """Grids of 1-5 cells along X: below 4 cells the X-pencil masks the out-of-run halves of a
     run's end pairs (their partner records can then be within r_c across a row end)."""
@@ -207,3 +207,20 @@ def test_narrow_x(nx, kernel):
     for algo in ALGOS:
         got, _ = gpu_interact(c, algo, kernel)
         assert_parity(got, want, label=f"nx={nx} {kernel} {algo}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_lj_softening_coincident_and_params(algo):
+    """Eq. (1) with softening (R19): coincident distinct particles interact through K(eps) with no
+    force; an isolated particle is exactly 0; non-default r, eps, E0 reach every strategy."""
+    grid = synth.Grid(dims=(4, 4, 4), w=0.25, lj_r=0.25, lj_eps=0.125, lj_e0=2.0)
+    c = synth.Cloud(grid, np.array([0.3, 0.3, 0.9], np.float32), np.array([0.3, 0.3, 0.9], np.float32),
+                    np.array([0.3, 0.3, 0.9], np.float32), np.array([2.0, 3.0, 1.0], np.float32))
+    got, _ = gpu_interact(c, algo, "lj")
+    K = 4 * 2.0 * (0.5 ** 12 - 0.5 ** 6)
+    assert got[0, 0] == pytest.approx(3.0 * K, rel=1e-6) and got[1, 0] == pytest.approx(2.0 * K, rel=1e-6)
+    assert np.all(got[:2, 1:] == 0) and np.all(got[2] == 0)
+    c2 = synth.scaled_uniform(8, (10, 8, 6), seed=21)
+    c2.grid = synth.Grid(dims=c2.grid.dims, w=c2.grid.w, lj_r=0.8 * c2.grid.w, lj_eps=0.03 * c2.grid.w, lj_e0=0.7)
+    got, _ = gpu_interact(c2, algo, "lj")
+    assert_parity(got, oracle_interact(c2, "lj"), label=f"lj params {algo}")

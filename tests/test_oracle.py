@@ -228,7 +228,7 @@ def test_lattice_closed_form(d):
         assert np.allclose(b["out"], r["out"], rtol=1e-12, atol=1e-12)
 
 
-@pytest.mark.parametrize("kernel", [ref.KERNEL_GAUSSIAN, ref.KERNEL_INDICATOR, ref.KERNEL_CANDIDATE])
+@pytest.mark.parametrize("kernel", [ref.KERNEL_GAUSSIAN, ref.KERNEL_INDICATOR, ref.KERNEL_CANDIDATE, ref.KERNEL_LJ])
 def test_celllist_equals_brute_force(kernel):
     """Cell-list oracle == O(N^2) brute force on configs[0] (N = 4096): identical pair sets and
     counts, sums to 1e-12."""
@@ -309,6 +309,79 @@ def test_force_is_minus_gradient():
             Xm = Xf.copy(); Xm[i, a] -= h
             g = (U(Xp) - U(Xm)) / (2 * h)
             assert -g == pytest.approx(r["out"][i, 1 + a], rel=1e-5, abs=1e-8)
+
+
+# ---------------------------------------------------------------- Lennard-Jones (Eq. (1), R19)
+
+def test_lj_hand_values():
+    """Eq. (1) as printed worked by hand at dyadic values: r = 1, eps = 0, E0 = 1,
+    d = 1/2 -> u^2 = 1/4: K = 4 (1/4096 - 1/64) = -252/4096; -dK/dd / d = -4 (12 u^10 - 6 u^4) =
+    -4 (12/1024 - 6/16) = 93/64 = 1.453125, so the force on particle 0 from particle 1 (at +1/2
+    along x) is q0 q1 * 1.453125 * (-1/2)."""
+    grid = synth.Grid(dims=(2, 2, 2), w=1.0, lj_r=1.0, lj_eps=0.0, lj_e0=1.0)
+    f = np.float32
+    x, y, z = np.array([0.25, 0.75], f), np.array([0.5, 0.5], f), np.array([0.5, 0.5], f)
+    q = np.array([1.5, 0.5], f)
+    for r in (ref.brute_force(x, y, z, q, grid, kernel=ref.KERNEL_LJ),
+              celllist.interact(x, y, z, q, grid, kernel=ref.KERNEL_LJ)):
+        o = r["out"]
+        assert o[0, 0] == -252.0 / 4096.0 * 0.5 and o[1, 0] == -252.0 / 4096.0 * 1.5
+        assert o[0, 1] == 1.5 * 0.5 * 1.453125 * -0.5 and o[1, 1] == -o[0, 1]
+        assert np.all(o[:, 2:] == 0)
+
+
+def test_lj_softening_and_isolated():
+    """Coincident distinct particles: d~ = eps, K(eps) = 4 E0 ((eps/r)^12 - (eps/r)^6), no force;
+    an isolated particle gets exactly 0 (identity exclusion)."""
+    grid = synth.Grid(dims=(4, 4, 4), w=0.25, lj_r=0.25, lj_eps=0.125, lj_e0=2.0)
+    f = np.float32
+    x = np.array([0.3, 0.3, 0.9], f)
+    q = np.array([2.0, 3.0, 1.0], f)
+    r = celllist.interact(x, x, x, q, grid, kernel=ref.KERNEL_LJ)
+    K = 4 * 2.0 * (0.5 ** 12 - 0.5 ** 6)
+    assert r["out"][0, 0] == 3.0 * K and r["out"][1, 0] == 2.0 * K
+    assert np.all(r["out"][:2, 1:] == 0) and np.all(r["out"][2] == 0)
+
+
+def test_lj_force_is_minus_gradient():
+    """F_i = -dU/dx_i, U = sum_{i<j} q_i q_j K(d~_ij), central differences (pairs away from r_c)."""
+    grid = synth.Grid(dims=(3, 3, 3), w=1.0 / 3, lj_r=0.3, lj_eps=0.02, lj_e0=1.5)
+    rng = np.random.default_rng(12)
+    n = 40
+    Xf = (rng.random((n, 3)) * 0.6 + 0.2).astype(np.float32).astype(np.float64)
+    q = rng.uniform(0.5, 1.5, n).astype(np.float32).astype(np.float64)
+    lr, le, l0 = ref.lj_params(grid)
+    rc2 = float(np.float32(grid.r_c)) ** 2
+
+    def U(Xa):
+        d = Xa[:, None, :] - Xa[None, :, :]
+        r2 = (d * d).sum(-1)
+        m = (r2 < rc2) & np.triu(np.ones((n, n), bool), 1)
+        dt = np.sqrt(r2 + le * le)  # the softened distance, written out (not lj_terms)
+        return (q[:, None] * q[None, :] * 4 * l0 * ((dt / lr) ** 12 - (dt / lr) ** 6) * m).sum()
+
+    d = Xf[:, None, :] - Xf[None, :, :]
+    r2 = (d * d).sum(-1)
+    np.fill_diagonal(r2, 0)
+    far = np.abs(r2 - rc2) > 1e-4
+    np.fill_diagonal(far, True)
+    ok = [i for i in range(n) if far[i].all()]
+    assert len(ok) >= 3
+    r = ref.brute_force(Xf[:, 0].astype(np.float32), Xf[:, 1].astype(np.float32), Xf[:, 2].astype(np.float32),
+                        q.astype(np.float32), grid, kernel=ref.KERNEL_LJ)
+    h = 1e-6
+    for i in ok[:6]:
+        for a in range(3):
+            Xp = Xf.copy(); Xp[i, a] += h
+            Xm = Xf.copy(); Xm[i, a] -= h
+            g = (U(Xp) - U(Xm)) / (2 * h)
+            assert -g == pytest.approx(r["out"][i, 1 + a], rel=1e-5, abs=1e-7)
+
+
+def test_lj_antisymmetry():
+    c = synth.make_config("c0")
+    r = celllist.interact(c.x, c.y, c.z, c.q, c.grid, kernel=ref.KERNEL_LJ)
+    assert np.all(np.abs(r["out"][:, 1:].sum(0)) <= 1e-12 * r["S"][:, 1:].sum(0))
 
 
 # ---------------------------------------------------------------- paper's in-SM scan

@@ -18,8 +18,11 @@ __global__ void __launch_bounds__(NT) k(float *out, int reps, int wpairs, long l
   float acc = 0.f;
   for (int r = 0; r < reps; ++r) {
     const int p0 = ((threadIdx.x >> 3) * 37 * 4 + r * 4 * 101 + (threadIdx.x & 24) / 8) % (npairs - wpairs - 8);
-    float4 v = lane_target<PI_K_GAUSSIAN, UNR>(S, p0 + 3, threadIdx.x & 1, p0, p0 + wpairs, 2.4e-4f, -6.5f / 2.4e-4f);
-    acc += v.x + v.y + v.z + v.w;
+    const float xt = S[2 * p0].x, yt = S[2 * p0].z, zt = S[2 * p0 + 1].x;
+    p2 ph = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
+    for (int q = p0; q < p0 + wpairs; ++q)
+      src_eval<PI_K_GAUSSIAN>(load_pair(S, q), xt, yt, zt, 2.4e-4f, -6.5f / 2.4e-4f, ph, fx, fy, fz);
+    acc += lo(ph) + hi(fx) + lo(fy) + hi(fz);
   }
   long long t1 = clock64();
   out[blockIdx.x * NT + threadIdx.x] = acc;
