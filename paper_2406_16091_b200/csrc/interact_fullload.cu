@@ -308,19 +308,40 @@ cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const Inte
   p.kp = k;
   p.out = a.out;
   p.ctl = a.ctl;
-  p.bx = a.fb[0] > 0 ? a.fb[0] : 8;
-  p.by = a.fb[1] > 0 ? a.fb[1] : 4;
-  p.bz = a.fb[2] > 0 ? a.fb[2] : 4;
+  const double ppc = (double)a.n_est / (double)g.ncells;
+  const size_t max_smem = 227 * 1024;
+  if (a.fb[0] > 0 || a.fb[1] > 0 || a.fb[2] > 0) {
+    p.bx = a.fb[0] > 0 ? a.fb[0] : 8;
+    p.by = a.fb[1] > 0 ? a.fb[1] : 4;
+    p.bz = a.fb[2] > 0 ? a.fb[2] : 4;
+  } else {
+    // the sub-box from the density (the paper sizes it from M_C):
+    // the largest of these whose staged cells hold the mean occupancy (+25 %) in shared memory
+    static const int boxes[][3] = {{8, 4, 4}, {4, 4, 4}, {4, 4, 2}, {4, 2, 2}, {2, 2, 2}, {2, 2, 1}, {2, 1, 1},
+                                   {1, 1, 1}};
+    // ... and, as the paper's shrink rule (:270-276), small enough for two blocks per SM
+    int k = 0;
+    const long long nblk_min = 2LL * 148;
+    for (; k < 7; ++k) {
+      const double st = (double)(boxes[k][0] + 2) * (boxes[k][1] + 2) * (boxes[k][2] + 2);
+      const long long nblk = (long long)((g.own_hi - g.own_lo + boxes[k][0] - 1) / boxes[k][0]) *
+                             ((g.ny + boxes[k][1] - 1) / boxes[k][1]) * ((g.nz + boxes[k][2] - 1) / boxes[k][2]);
+      if (fl_smem_bytes(boxes[k][0], boxes[k][1], boxes[k][2], (int)(st * ppc * 1.25 + 64.0)) <= max_smem &&
+          nblk >= nblk_min)
+        break;
+    }
+    p.bx = boxes[k][0];
+    p.by = boxes[k][1];
+    p.bz = boxes[k][2];
+  }
   p.bx = min(p.bx, g.own_hi - g.own_lo);
   p.by = min(p.by, g.ny);
   p.bz = min(p.bz, g.nz);
   // fewer than 27 staged cells cannot hold one target cell and its ghosts;
   // with the ghost shell always included here the smallest box is 1x1x1 (+ shell = 27 cells)
-  const double ppc = (double)a.n_est / (double)g.ncells;
   const double staged = (double)(p.bx + 2) * (p.by + 2) * (p.bz + 2);
   p.cap = a.fb_cap > 0 ? a.fb_cap : (int)(staged * ppc * 1.25 + 64.0);
   p.cap = (p.cap + 31) & ~31;
-  const size_t max_smem = 227 * 1024;
   if (fl_smem_bytes(p.bx, p.by, p.bz, 64) > max_smem) return cudaErrorNotSupported;
   while (fl_smem_bytes(p.bx, p.by, p.bz, p.cap) > max_smem && p.cap > 64) p.cap -= 32;
   const int threads = a.threads == 128 ? 128 : (a.threads == 512 ? 512 : 256);
