@@ -180,7 +180,7 @@ __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, 
   const float4 *__restrict__ S = sl.S;
   p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
   p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
-#pragma unroll 1
+#pragma unroll  // the 9 runs unrolled: their bounds loads schedule early (measured: -1 %)
   for (int r = 0; r < 9; ++r) {
     const int a = sl.O[r * LF + klo], b = sl.O[r * LF + khi + 1];
     if (b <= a) continue;
