@@ -18,7 +18,7 @@ constexpr size_t ALIGN = 256;
 size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-  size_t ctl, counts, offsets, foffsets, tiles, rec, sid, perm, urec, uid, rank, outs, io, pairs;
+  size_t ctl, counts, offsets, foffsets, pcounts, tiles, rec, sid, perm, urec, uid, rank, outs, io, pairs;
   size_t xrec, xid, xperm, msg[4];  // nranks > 1
   size_t total;
 };
@@ -71,6 +71,7 @@ Layout make_layout(const pi_config *cfg) {
   L.counts = take(sizeof(int32_t) * (size_t)(nf + 4));
   L.offsets = take(sizeof(int32_t) * (size_t)(ncells + 4));
   L.foffsets = take(sizeof(int32_t) * (size_t)(nf + 4));
+  L.pcounts = take(sizeof(int32_t) * (size_t)(nf + 4));
   L.tiles = take(sizeof(unsigned long long) * (size_t)scan_tiles(nf));
   L.rec = take(sizeof(float4) * (size_t)cap);
   L.sid = take(sizeof(int32_t) * (size_t)cap);
@@ -152,7 +153,7 @@ struct pi_ctx_s {
   Layout lay;
   unsigned char *ws;
   DevCtl *ctl;
-  int32_t *counts, *offsets, *foffsets, *sid, *perm, *uid, *rank;
+  int32_t *counts, *offsets, *foffsets, *pcounts, *sid, *perm, *uid, *rank;
   unsigned long long *tiles;
   float4 *rec, *urec, *outs, *pairs;
   float *io;
@@ -160,6 +161,7 @@ struct pi_ctx_s {
   int state;         // 0 empty, 1 binned from pi_bin, 2 sorted state from pi_step (update pending)
   bool need_bin;     // pi_step must re-bin (and, nranks > 1, migrate) first
   bool pairs_ready;  // c->pairs hold the sorted records as source pairs (written by the AoS scatter)
+  bool pcounts_ok;   // pcounts = per-sub-cell counts of the current sorted state (one rank)
   bool interacted;
   long long steps;
   SlabState slab;    // nranks > 1
@@ -264,6 +266,7 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   c->counts = reinterpret_cast<int32_t *>(c->ws + lay.counts);
   c->offsets = reinterpret_cast<int32_t *>(c->ws + lay.offsets);
   c->foffsets = reinterpret_cast<int32_t *>(c->ws + lay.foffsets);
+  c->pcounts = reinterpret_cast<int32_t *>(c->ws + lay.pcounts);
   c->tiles = reinterpret_cast<unsigned long long *>(c->ws + lay.tiles);
   c->rec = reinterpret_cast<float4 *>(c->ws + lay.rec);
   c->sid = reinterpret_cast<int32_t *>(c->ws + lay.sid);
@@ -286,6 +289,8 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   g.own_lo = sg.own_lo;
   g.own_hi = sg.own_hi;
   g.sx = x_subcells(cfg);
+  g.sxs = 0;
+  while ((1 << g.sxs) < g.sx) ++g.sxs;
   g.lx = g.ox; g.ly = g.oy; g.lz = g.oz;
   g.hx = g.ox + (float)cfg->dims[0] * g.w;
   g.hy = g.oy + (float)g.ny * g.w;
@@ -380,8 +385,14 @@ pi_status pi_set_tuning(pi_ctx c, const pi_tuning *t) {
 
 // a1-a4 on SoA input (x != NULL) or on AoS records.
 static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, const float *z, const float *q,
-                        const int32_t *id, const float4 *rec_in, const int32_t *perm_in, const long long *n_dev) {
+                        const int32_t *id, const float4 *rec_in, const int32_t *perm_in, const long long *n_dev,
+                        bool delta = false) {
   BinArgs a{};
+  const bool one = c->cfg.nranks == 1;
+  a.delta = delta;
+  // the SoA path's scan records the persistent counts; the delta path re-bins from them
+  a.pcounts = one && (delta || !rec_in) ? c->pcounts : nullptr;
+  c->pcounts_ok = one && (delta || !rec_in);
   a.n = n;
   a.n_dev = n_dev;
   a.x = x; a.y = y; a.z = z; a.q = q;
@@ -468,6 +479,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.out.sid = c->sid;
   a.out.uid = c->uid;
   a.out.dt = dt;
+  if (integrate && c->pcounts_ok) a.out.pcounts = c->pcounts;  // movers update the persistent counts
   a.tx_len = c->tune.xpencil_len;
   a.tx_cap = c->tune.xpencil_cap;
   a.threads = c->tune.threads;
@@ -524,7 +536,7 @@ pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
       phase_end(c, 2);
       s = slab_ghosts_and_bin(c);
     } else {
-      s = do_bin(c, c->n, nullptr, nullptr, nullptr, nullptr, c->uid, c->urec, nullptr, nullptr);
+      s = do_bin(c, c->n, nullptr, nullptr, nullptr, nullptr, c->uid, c->urec, nullptr, nullptr, c->pcounts_ok);
     }
     if (s != PI_OK) return s;
   }

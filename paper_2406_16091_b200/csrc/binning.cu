@@ -167,11 +167,15 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
 // The scan runs over the FINE counts (X sub-cells, sx per cell; sx divides SCAN_ITEMS, so a
 // thread's items are whole cells): it writes the fine offsets (the sorted order) and every
 // sx-th of them as the per-cell offsets; M_C is the largest per-cell sum.
-template <bool KEEP>  // KEEP: leave the counts (the scatter consumes them)
+// KEEP: leave the counts (the scatter consumes them);  copy: nullable, receives the counts read
+// (pi_bin: the persistent counts of the new sorted state; delta re-binning: the scatter's copy).
+template <bool KEEP>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t *__restrict__ counts,
                                                        int32_t *__restrict__ offsets,
                                                        unsigned long long *__restrict__ status, int num_tiles,
-                                                       DevCtl *ctl, int sx, int32_t *__restrict__ cell_offsets) {
+                                                       DevCtl *ctl, int sxs, int32_t *__restrict__ cell_offsets,
+                                                       int32_t *__restrict__ copy) {
+  const int sx = 1 << sxs;
   __shared__ int s_tile;
   __shared__ int s_warp[SCAN_THREADS / 32];
   __shared__ int s_prefix;
@@ -194,6 +198,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
       int4 a = p[k];
       v[4 * k] = a.x; v[4 * k + 1] = a.y; v[4 * k + 2] = a.z; v[4 * k + 3] = a.w;
       if (!KEEP) p[k] = make_int4(0, 0, 0, 0);  // leave zeroed counts for the next binning
+      if (copy) reinterpret_cast<int4 *>(copy + base)[k] = a;
     }
   } else {
 #pragma unroll
@@ -201,6 +206,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
       long long c = base + k;
       v[k] = c < ncells ? counts[c] : 0;
       if (!KEEP && c < ncells) counts[c] = 0;
+      if (copy && c < ncells) copy[c] = v[k];
     }
   }
   int mx = 0, sum = 0, grp = 0;
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
   for (int k = 0; k < SCAN_ITEMS; ++k) {
     sum += v[k];
     grp += v[k];
-    if ((k + 1) % sx == 0) {  // end of a cell
+    if (((k + 1) & (sx - 1)) == 0) {  // end of a cell
       mx = max(mx, grp);
       grp = 0;
     }
@@ -284,10 +290,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
   }
 #pragma unroll
   for (int k = 0; k < SCAN_ITEMS; k += 1)  // per-cell offsets: every sx-th fine offset
-    if (k % sx == 0 && base + k < ncells) cell_offsets[(base + k) / sx] = outv[k];
+    if ((k & (sx - 1)) == 0 && base + k < ncells) cell_offsets[(base + k) >> sxs] = outv[k];
   if (base <= ncells - 1 && ncells - 1 < base + SCAN_ITEMS) {  // offsets[Nc] = N
     offsets[ncells] = run;
-    cell_offsets[ncells / sx] = run;
+    cell_offsets[ncells >> sxs] = run;
   }
   // last block: publish M_C, reset counters, advance the epoch
   __syncthreads();
@@ -380,13 +386,24 @@ int grid_for(long long work, int threads) {
 int scan_tiles(long long nitems) { return (int)((nitems + SCAN_TILE - 1) / SCAN_TILE); }
 
 cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
+  if (a.delta) {  // pi_step re-binning from the persistent counts: no count pass
+    const long long nf0 = g.ncells * g.sx;
+    const int tiles0 = scan_tiles(nf0);
+    k_scan<true><<<tiles0, SCAN_THREADS, 0, s>>>(nf0, a.pcounts, a.foffsets, a.tile_status, tiles0, a.ctl, g.sxs,
+                                                 a.offsets, a.counts);
+    if (a.n > 0)
+      k_scatter<true, true><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
+          a.n, nullptr, nullptr, nullptr, nullptr, a.rec_in, a.id_in, g, a.counts, a.foffsets, a.rec_out, a.sid_out,
+          a.perm_out, a.perm_in, a.n_dev, reinterpret_cast<float *>(a.pairs_out));
+    return cudaGetLastError();
+  }
   const long long nf = g.ncells * g.sx;  // fine cells
   const int tiles = scan_tiles(nf);
   if (a.rec_in) {  // AoS: count, scan keeping the counts, scatter taking ranks from them
     if (a.n > 0)
       k_count_aos<<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.rec_in, g, a.counts, a.ctl, a.n_dev);
-    k_scan<true><<<tiles, SCAN_THREADS, 0, s>>>(nf, a.counts, a.foffsets, a.tile_status, tiles, a.ctl, g.sx,
-                                                a.offsets);
+    k_scan<true><<<tiles, SCAN_THREADS, 0, s>>>(nf, a.counts, a.foffsets, a.tile_status, tiles, a.ctl, g.sxs,
+                                                a.offsets, nullptr);
     if (a.n > 0)
       k_scatter<true, true><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
           a.n, nullptr, nullptr, nullptr, nullptr, a.rec_in, a.id_in, g, a.counts, a.foffsets, a.rec_out, a.sid_out,
@@ -397,8 +414,8 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
   if (a.n > 0)
     k_count_soa<<<grid_for((a.n + 3) / 4, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.x, a.y, a.z, g, a.counts,
                                                                                  a.rank, a.cell_of, a.ctl);
-  k_scan<false><<<tiles, SCAN_THREADS, 0, s>>>(nf, a.counts, a.foffsets, a.tile_status, tiles, a.ctl, g.sx,
-                                                 a.offsets);
+  k_scan<false><<<tiles, SCAN_THREADS, 0, s>>>(nf, a.counts, a.foffsets, a.tile_status, tiles, a.ctl, g.sxs,
+                                                 a.offsets, a.pcounts);
   if (a.n > 0)
     k_scatter<false><<<grid_for(a.n, COUNT_THREADS), COUNT_THREADS, 0, s>>>(
         a.n, a.x, a.y, a.z, a.q, nullptr, a.id_in, g, a.rank, a.foffsets, a.rec_out, a.sid_out, a.perm_out, nullptr,

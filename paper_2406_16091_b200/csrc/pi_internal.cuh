@@ -18,7 +18,7 @@ struct Geom {
   int gnx;            // global dims[0]
   int gx_off;         // global X index of local X cell 0 (-1 + rank * Lx when nranks > 1)
   int own_lo, own_hi; // owned local X cells [own_lo, own_hi): targets of the interaction
-  int sx;             // X sub-cells per cell of the binning order (1, 2, 4, 8, 16)
+  int sx, sxs;        // X sub-cells per cell of the binning order (1, 2, 4, 8, 16), sx = 1 << sxs
   float hx, hy, hz;   // upper faces of the global box (integration walls)
   float lx, ly, lz;   // lower faces
 };
@@ -95,18 +95,18 @@ __device__ __forceinline__ int fine_x_global(const Geom &g, float x, bool &bad) 
   bad |= !(f == f);
   const int c = (f >= 0.f) ? ((f < (float)g.gnx) ? (int)f : g.gnx - 1) : 0;
   const int sub = min(max((int)((t - (float)c) * (float)g.sx), 0), g.sx - 1);
-  return c * g.sx + sub;
+  return (c << g.sxs) + sub;
 }
 
 // Linear FINE cell (the binning order): X sub-cell fastest inside the cell, then the cell
 // linearisation; cells outside the local slab clamp into the ghost layers like cell_lin.
 __device__ __forceinline__ int fine_lin(const Geom &g, float x, float y, float z, bool &bad) {
   const int fg = fine_x_global(g, x, bad);
-  const int cl = fg / g.sx - g.gx_off;
-  const int fx = cl < 0 ? 0 : (cl >= g.nx ? g.nx * g.sx - 1 : cl * g.sx + (fg - (fg / g.sx) * g.sx));
+  const int cl = (fg >> g.sxs) - g.gx_off;
+  const int fx = cl < 0 ? 0 : (cl >= g.nx ? (g.nx << g.sxs) - 1 : (cl << g.sxs) + (fg & (g.sx - 1)));
   const int cy = cell_coord(y, g.oy, g.inv_w, g.ny, bad);
   const int cz = cell_coord(z, g.oz, g.inv_w, g.nz, bad);
-  return fx + g.nx * g.sx * (cy + g.ny * cz);
+  return fx + ((g.nx * (cy + g.ny * cz)) << g.sxs);
 }
 
 __device__ __forceinline__ float ex2_approx(float a) {
@@ -143,6 +143,9 @@ struct OutDesc {
   const int32_t *sid;
   int32_t *uid;
   float dt;
+  // persistent per-sub-cell counts of the sorted state (nullable): a particle whose fine cell
+  // changes in the update moves one count from its old to its new fine cell
+  int32_t *pcounts;
 };
 
 __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, int t, float4 rec, float phi,
@@ -165,6 +168,14 @@ __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, in
     u.w = rec.w;
     o.upd[t] = u;
     o.uid[t] = o.sid[t];
+    if (o.pcounts) {
+      bool bad = false;
+      const int f0 = fine_lin(g, rec.x, rec.y, rec.z, bad), f1 = fine_lin(g, u.x, u.y, u.z, bad);
+      if (f1 != f0) {
+        atomicSub(o.pcounts + f0, 1);
+        atomicAdd(o.pcounts + f1, 1);
+      }
+    }
   }
 }
 
@@ -190,6 +201,8 @@ struct BinArgs {
   const int32_t *perm_in;       // AoS path: input index per record (-1 = ghost), or NULL
   float4 *pairs_out;            // AoS path, nullable: also write the sorted records as f32x2
                                 // source pairs (layout of InteractArgs::pairs)
+  int32_t *pcounts;             // [ncells sx] persistent counts of the sorted state (one rank)
+  bool delta;                   // AoS re-binning from pcounts (kept current by the pi_step update)
   DevCtl *ctl;
 };
 
