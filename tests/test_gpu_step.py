@@ -8,7 +8,7 @@ import torch
 import synth
 from oracle import celllist
 from oracle import reference as ref
-from tests._util import assert_parity, ctx_for, to_dev
+from tests._util import KERNEL_ID, assert_parity, ctx_for, to_dev
 
 pytestmark = pytest.mark.gpu
 
@@ -19,14 +19,21 @@ def state(ctx):
     return {k: v.cpu().numpy() for k, v in p.items()}
 
 
-@pytest.mark.parametrize("algo", ["global", "xpencil", "fullload"])
-def test_step_matches_oracle(algo):
+@pytest.mark.parametrize("algo,kernel,xs", [("global", "gaussian", 0), ("xpencil", "gaussian", 0),
+                                             ("fullload", "gaussian", 0), ("xpencil", "gaussian", 1),
+                                             ("xpencil", "gaussian", 8), ("xpencil", "lj", 0),
+                                             ("global", "lj", 4)])
+def test_step_matches_oracle(algo, kernel, xs):
+    """Three steps, each checked against the oracle at the GPU's pre-step state; the re-binning
+    (counts carried by the update, R18 sub-cells) must be bit-exact per cell afterwards."""
     c = synth.make_config("c0")
     g = c.grid
-    ctx = ctx_for(c)
+    ctx = ctx_for(c, kernel, x_subcells=xs)
     ctx.bin(*to_dev(c))
     s0 = state(ctx)                                   # sorted state before the step
-    dt = np.float32(1e-5)
+    # dt: a few % of the particles change sub-cell each step (the Gaussian forces of c0 are
+    # ~1e2, LJ's ~1e4)
+    dt = np.float32(1e-5 if kernel == "gaussian" else 1e-7)
     for it in range(3):
         ctx.step(algo, float(dt))
         s1 = state(ctx)                               # updated positions + this step's outputs
@@ -34,7 +41,7 @@ def test_step_matches_oracle(algo):
         order0 = np.argsort(s0["id"])
         order1 = np.argsort(s1["id"])
         X0 = [s0[k][order0] for k in ("x", "y", "z", "q")]
-        want = celllist.interact(*X0, g)
+        want = celllist.interact(*X0, g, kernel=KERNEL_ID[kernel])
         got = np.stack([s1[k][order1] for k in ("phi", "fx", "fy", "fz")], 1).astype(np.float64)
         assert_parity(got, want, label=f"step{it} forces")
         # position update: x + dt F, reflected, from the GPU's own forces (fp32 fma -> 1 ulp)
