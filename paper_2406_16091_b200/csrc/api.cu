@@ -162,6 +162,7 @@ struct pi_ctx_s {
   bool need_bin;     // pi_step must re-bin (and, nranks > 1, migrate) first
   bool pairs_ready;  // c->pairs hold the sorted records as source pairs (written by the AoS scatter)
   bool pcounts_ok;   // pcounts = per-sub-cell counts of the current sorted state (one rank)
+  bool rec_ok;       // rec holds the current sorted records (else only the pair array does)
   bool interacted;
   long long steps;
   SlabState slab;    // nranks > 1
@@ -386,7 +387,7 @@ pi_status pi_set_tuning(pi_ctx c, const pi_tuning *t) {
 // a1-a4 on SoA input (x != NULL) or on AoS records.
 static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, const float *z, const float *q,
                         const int32_t *id, const float4 *rec_in, const int32_t *perm_in, const long long *n_dev,
-                        bool delta = false) {
+                        bool delta = false, bool pairs_only = false) {
   BinArgs a{};
   const bool one = c->cfg.nranks == 1;
   a.delta = delta;
@@ -404,7 +405,8 @@ static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, c
   a.offsets = c->offsets;
   a.foffsets = c->foffsets;
   a.tile_status = c->tiles;
-  a.rec_out = c->rec;
+  a.rec_out = (pairs_only && rec_in) ? nullptr : c->rec;  // pi_step + X-pencil: pairs only
+  c->rec_ok = a.rec_out != nullptr;
   a.sid_out = c->sid;
   a.perm_out = (rec_in && !perm_in) ? nullptr : c->perm;
   a.perm_in = perm_in;
@@ -466,7 +468,9 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.n = multi ? c->cfg.capacity : c->n;
   a.n_dev = multi ? &c->ctl->n_total : nullptr;
   a.n_est = multi ? c->n * (long long)(c->slab.Lx + 2) / (c->slab.Lx > 0 ? c->slab.Lx : 1) : c->n;
-  a.rec = c->rec;
+  if (!c->rec_ok && algo != PI_A_XPENCIL && algo != PI_A_AUTO)
+    return fail(c, PI_ESTATE, "internal: sorted records not materialised for this strategy");
+  a.rec = c->rec_ok ? c->rec : nullptr;
   a.foffsets = c->foffsets;
   a.pairs = c->pairs;
   a.pairs_ready = c->pairs_ready;
@@ -536,7 +540,9 @@ pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
       phase_end(c, 2);
       s = slab_ghosts_and_bin(c);
     } else {
-      s = do_bin(c, c->n, nullptr, nullptr, nullptr, nullptr, c->uid, c->urec, nullptr, nullptr, c->pcounts_ok);
+      // the X-pencil reads only the pair array: the records need not be written (16 B/particle)
+      s = do_bin(c, c->n, nullptr, nullptr, nullptr, nullptr, c->uid, c->urec, nullptr, nullptr, c->pcounts_ok,
+                 algo == PI_A_XPENCIL || algo == PI_A_AUTO);
     }
     if (s != PI_OK) return s;
   }

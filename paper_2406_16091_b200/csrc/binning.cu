@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
       rk = __ldg(rank + i);
     }
     int slot = __ldg(offsets + lin) + rk;  // fine offsets
-    rec_out[slot] = r;
+    if (rec_out) rec_out[slot] = r;       // (pi_step with the X-pencil: the pair array only)
     if (pairs_out) {  // f32x2 source-pair layout: P[2k] = (x0, x1, y0, y1), P[2k+1] = (z0, z1, q0, q1)
       float *pp = pairs_out + 8 * (long long)(slot >> 1) + (slot & 1);
       pp[0] = r.x;

@@ -198,12 +198,22 @@ __device__ __forceinline__ void scalar_term(const KParams &kp, float r2, float q
 
 // Fallback for a target whose cell window does not fit the staging buffer: Par-Part-NoLoop
 // over global memory (Alg. 1) for target slot t in cell (cx, cy, cz).
-template <int KERNEL>
+// Record s of the sorted state: from the records, or (rec == NULL) from the f32x2 pair array
+// P[2k] = (x_2k, x_2k+1, y_2k, y_2k+1), P[2k+1] = (z.., z.., q.., q..).
+__device__ __forceinline__ float4 sorted_rec(const float4 *__restrict__ rec, const float4 *__restrict__ pairs,
+                                             int s) {
+  if (rec) return __ldg(rec + s);
+  const float4 a = __ldg(pairs + 2 * (s >> 1)), b = __ldg(pairs + 2 * (s >> 1) + 1);
+  return (s & 1) ? make_float4(a.y, a.w, b.y, b.w) : make_float4(a.x, a.z, b.x, b.z);
+}
+
+template <int KERNEL, bool UPD = true>
 __device__ void fallback_target(int t, int cx, int cy, int cz, const float4 *__restrict__ rec,
                                 const int32_t *__restrict__ offsets, const Geom &g, const KParams &kp,
-                                const OutDesc &out, unsigned long long &cand) {
+                                const OutDesc &out, unsigned long long &cand,
+                                const float4 *__restrict__ pairs = nullptr) {
   const int xlo = max(cx - 1, 0), xhi = min(cx + 1, g.nx - 1);
-  const float4 me = __ldg(rec + t);
+  const float4 me = sorted_rec(rec, pairs, t);
   float phi = 0.f, fx = 0.f, fy = 0.f, fz = 0.f;
   for (int dz = -1; dz <= 1; ++dz) {
     const int z = cz + dz;
@@ -216,7 +226,7 @@ __device__ void fallback_target(int t, int cx, int cy, int cz, const float4 *__r
       cand += (unsigned long long)(hi_ - lo_);
       for (int s = lo_; s < hi_; ++s) {
         if (s == t) continue;
-        const float4 o = __ldg(rec + s);
+        const float4 o = sorted_rec(rec, pairs, s);
         const float dx = me.x - o.x, dy2 = me.y - o.y, dz2 = me.z - o.z;
         const float r2 = fmaf(dz2, dz2, fmaf(dy2, dy2, dx * dx));
         if (KERNEL == PI_K_CANDIDATE) {
@@ -244,7 +254,7 @@ __device__ void fallback_target(int t, int cx, int cy, int cz, const float4 *__r
   } else {
     fx = fy = fz = 0.f;
   }
-  write_output(out, g, t, me, phi, fx, fy, fz);
+  write_output<UPD>(out, g, t, me, phi, fx, fy, fz);
 }
 
 }  // namespace pi

@@ -224,7 +224,7 @@ __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, 
                      lo(fz) + hi(fz));
 }
 
-template <int KERNEL, int NC>
+template <int KERNEL, int NC, bool UPD>  // UPD: pi_step (update + carried counts in the epilogue)
 __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem_raw);  // [NSLOT]
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         if (T < ntargets) {
           const int gs = t0 + T;
           if (jb < ja) {  // fallback round: cell ja from global memory
-            fallback_target<KERNEL>(gs, x0 - 1 + ja, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand);
+            fallback_target<KERNEL, UPD>(gs, x0 - 1 + ja, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand, p.pairs);
             if (T == 0) ++fallbacks;
           } else {
             // cell of the target: last j in [ja, jb] with O4[j sx] <= gs
@@ -366,9 +366,9 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
             cand += (unsigned long long)(nc - 1);
             if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
               const float sc = -me.w * p.kp.f_ts;  // the walk summed wf (x_s - x_t)
-              write_output(p.out, g, gs, me, r.x * p.kp.phi_scale, sc * r.y, sc * r.z, sc * r.w);
+              write_output<UPD>(p.out, g, gs, me, r.x * p.kp.phi_scale, sc * r.y, sc * r.z, sc * r.w);
             } else {
-              write_output(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f);
+              write_output<UPD>(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f);
             }
           }
         }
@@ -410,11 +410,17 @@ cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
     kern<<<(int)blocks, (NC + 1) * 32, smem, s>>>(p);
     return cudaGetLastError();
   };
+  const bool upd = p.out.upd != nullptr;
   switch (p.kp.kernel) {
-    case PI_K_GAUSSIAN: return go(k_interact_xpencil<PI_K_GAUSSIAN, NC>);
-    case PI_K_INDICATOR: return go(k_interact_xpencil<PI_K_INDICATOR, NC>);
-    case PI_K_LJ: return go(k_interact_xpencil<PI_K_LJ, NC>);
-    default: return go(k_interact_xpencil<PI_K_CANDIDATE, NC>);
+    case PI_K_GAUSSIAN:
+      return upd ? go(k_interact_xpencil<PI_K_GAUSSIAN, NC, true>) : go(k_interact_xpencil<PI_K_GAUSSIAN, NC, false>);
+    case PI_K_INDICATOR:
+      return upd ? go(k_interact_xpencil<PI_K_INDICATOR, NC, true>)
+                 : go(k_interact_xpencil<PI_K_INDICATOR, NC, false>);
+    case PI_K_LJ: return upd ? go(k_interact_xpencil<PI_K_LJ, NC, true>) : go(k_interact_xpencil<PI_K_LJ, NC, false>);
+    default:
+      return upd ? go(k_interact_xpencil<PI_K_CANDIDATE, NC, true>)
+                 : go(k_interact_xpencil<PI_K_CANDIDATE, NC, false>);
   }
 }
 
@@ -457,11 +463,9 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  if (nc <= 4) return launch_nc<4>(p, s);
   if (nc <= 8) return launch_nc<8>(p, s);
   if (nc <= 16) return launch_nc<16>(p, s);
-  if (nc <= 20) return launch_nc<20>(p, s);
-  return launch_nc<24>(p, s);
+  return launch_nc<20>(p, s);
 }
 
 }  // namespace pi

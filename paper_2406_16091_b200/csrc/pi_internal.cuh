@@ -148,6 +148,8 @@ struct OutDesc {
   int32_t *pcounts;
 };
 
+// UPD = false compiles the pi_step update out (kernels specialised for pi_interact).
+template <bool UPD = true>
 __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, int t, float4 rec, float phi,
                                              float fx, float fy, float fz) {
   o.sorted[t] = make_float4(phi, fx, fy, fz);
@@ -160,7 +162,7 @@ __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, in
       if (o.fz) o.fz[c] = fz;
     }
   }
-  if (o.upd) {
+  if (UPD && o.upd) {
     float4 u;
     u.x = integrate1(rec.x, fx, o.dt, g.lx, g.hx);
     u.y = integrate1(rec.y, fy, o.dt, g.ly, g.hy);
@@ -195,7 +197,7 @@ struct BinArgs {
   int32_t *foffsets;            // [ncells sx + 1] per fine cell (the sorted order)
   unsigned long long *tile_status;
   int num_tiles_cap;
-  float4 *rec_out;              // sorted records (x, y, z, q)
+  float4 *rec_out;              // sorted records (x, y, z, q); NULL: only pairs_out (AoS path)
   int32_t *sid_out;             // sorted ids
   int32_t *perm_out;            // sorted slot -> input index (nullable)
   const int32_t *perm_in;       // AoS path: input index per record (-1 = ghost), or NULL
@@ -213,7 +215,7 @@ struct InteractArgs {
   long long n;                  // particles in the sorted state (upper bound if n_dev)
   const long long *n_dev;       // device-resident count (nranks > 1), or NULL
   long long n_est;              // host estimate of the sorted count (sizes staging buffers)
-  const float4 *rec;            // sorted records
+  const float4 *rec;            // sorted records (NULL when only the pair array is current)
   float4 *pairs;                // [2 * (n / 2 + 1)]: the records as f32x2 source pairs
   bool pairs_ready;             // pairs already hold the current sorted state (AoS binning)
   const int32_t *offsets;       // [ncells + 1]
