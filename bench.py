@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--config", default="c1")
     ap.add_argument("--algo", default="xpencil")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-binning-2e24", action="store_true", help="skip the 2^24 binning measurement")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -200,6 +201,52 @@ def run_reference(a):
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------ binning at 2^24
+def binning_at_scale(a, dev, stream, flush):
+    """The binning phase's HBM roofline at 2^24 particles, 128^3 cells (configs[2] ppc 8; configs[1]
+    is L2-resident): the pi_step re-binning (the method's steady state, nearly sorted input) and
+    the first pi_bin of random-order input, device time from the library's phase events."""
+    import statistics as st
+    import torch
+    import synth
+    from paper_2406_16091_b200 import Context
+    c = synth.make_config("c2_ppc8")
+    g = c.grid
+    ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=c.n, device=dev, stream=stream)
+    x, y, z, q = (torch.from_numpy(v).to(dev) for v in (c.x, c.y, c.z, c.q))
+    first = []
+    for _ in range(3):
+        flush.zero_()
+        ctx.bin(x, y, z, q)
+        first.append(ctx.stats()["bin_ms"])
+    _, fx, fy, fz = ctx.interact(a.algo)
+    fm = float(torch.stack([fx.abs().max(), fy.abs().max(), fz.abs().max()]).max())
+    dt = 0.01 * g.w / max(fm, 1e-30)
+    del fx, fy, fz
+    ctx.step(a.algo, dt)
+    rebin = []
+    for _ in range(8):
+        flush.zero_()
+        ctx.step(a.algo, dt)
+        rebin.append(ctx.stats()["bin_ms"])
+    ctx.close()
+    byts = 48.0 * c.n + 12.0 * g.ncells
+    peak = hbm_peak_gbs()
+    r_ms, f_ms = st.median(rebin), st.median(first)
+    return {"workload": "2^24 uniform particles, 128^3 cells (configs[2] ppc 8)", "bytes_model": "48 B/particle + 12 B/cell",
+            "rebin_ms": r_ms, "rebin_gbs": byts / (r_ms * 1e-3) / 1e9, "rebin_frac": byts / (r_ms * 1e-3) / 1e9 / peak,
+            "first_bin_ms": f_ms, "first_bin_gbs": byts / (f_ms * 1e-3) / 1e9,
+            "first_bin_frac": byts / (f_ms * 1e-3) / 1e9 / peak, "peak_gbs": peak,
+            "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy)"}
+
+
+def hbm_peak_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
 
 
 # ------------------------------------------------------------------------ our arm
@@ -370,6 +417,8 @@ def run_ours(a):
                                 "sample": f"{info['targets']} random targets of the {n}-particle cloud "
                                           f"({info['candidates']} candidates, {info['seconds']:.1f} s, fp64 C "
                                           "cell list incl. its own binning)"}
+    if world == 1 and not a.no_binning_2e24:
+        line["binning_2e24"] = binning_at_scale(a, dev, stream, flush)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

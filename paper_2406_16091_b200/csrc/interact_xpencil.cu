@@ -360,15 +360,23 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
             const int khi = KERNEL == PI_K_CANDIDATE ? (j + 2) * sx - 1 : min(max(fhi, (j - 1) * sx), (j + 2) * sx - 1);
             const float4 r = p.mask ? walk9<KERNEL, true>(sl, LF, sx, ja, klo, khi, me, thr, mc2, p.kp)
                                     : walk9<KERNEL, false>(sl, LF, sx, ja, klo, khi, me, thr, mc2, p.kp);
+            // the target's fine cell (sub-cell of its slot in the home pencil): moves of the
+            // update are counted against it without recomputing it from the position
+            int fold = -1;
+            if (UPD && p.out.pcounts) {
+              int sub = 0;
+              while (sub + 1 < sx && O4[j * sx + sub + 1] <= gs) ++sub;
+              fold = ((x0 - 1 + j) * sx + sub) + ((g.nx * (cy + g.ny * cz)) << g.sxs);
+            }
             int nc = 0;  // the 27-cell candidates (the unit of the metric, R4), pruned or not
 #pragma unroll
             for (int rr = 0; rr < 9; ++rr) nc += sl.O[rr * LF + (j + 2) * sx] - sl.O[rr * LF + (j - 1) * sx];
             cand += (unsigned long long)(nc - 1);
             if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
               const float sc = -me.w * p.kp.f_ts;  // the walk summed wf (x_s - x_t)
-              write_output<UPD>(p.out, g, gs, me, r.x * p.kp.phi_scale, sc * r.y, sc * r.z, sc * r.w);
+              write_output<UPD>(p.out, g, gs, me, r.x * p.kp.phi_scale, sc * r.y, sc * r.z, sc * r.w, fold);
             } else {
-              write_output<UPD>(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f);
+              write_output<UPD>(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f, fold);
             }
           }
         }

@@ -149,9 +149,10 @@ struct OutDesc {
 };
 
 // UPD = false compiles the pi_step update out (kernels specialised for pi_interact).
+// f_old: the target's fine cell if the caller knows it (else -1: computed from rec).
 template <bool UPD = true>
 __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, int t, float4 rec, float phi,
-                                             float fx, float fy, float fz) {
+                                             float fx, float fy, float fz, int f_old = -1) {
   o.sorted[t] = make_float4(phi, fx, fy, fz);
   if (o.perm) {
     const int c = o.perm[t];
@@ -172,7 +173,8 @@ __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, in
     o.uid[t] = o.sid[t];
     if (o.pcounts) {
       bool bad = false;
-      const int f0 = fine_lin(g, rec.x, rec.y, rec.z, bad), f1 = fine_lin(g, u.x, u.y, u.z, bad);
+      const int f0 = f_old >= 0 ? f_old : fine_lin(g, rec.x, rec.y, rec.z, bad);
+      const int f1 = fine_lin(g, u.x, u.y, u.z, bad);
       if (f1 != f0) {
         atomicSub(o.pcounts + f0, 1);
         atomicAdd(o.pcounts + f1, 1);
