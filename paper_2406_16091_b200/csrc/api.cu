@@ -18,7 +18,7 @@ constexpr size_t ALIGN = 256;
 size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-  size_t ctl, counts, offsets, foffsets, pcounts, tiles, rec, sid, perm, urec, uid, rank, outs, io, pairs;
+  size_t ctl, counts, offsets, foffsets, pcounts, tiles, bcur, rec, sid, perm, urec, uid, tidx, outs, io, pairs;
   size_t xrec, xid, xperm, msg[4];  // nranks > 1
   size_t total;
 };
@@ -73,12 +73,13 @@ Layout make_layout(const pi_config *cfg) {
   L.foffsets = take(sizeof(int32_t) * (size_t)(nf + 4));
   L.pcounts = take(sizeof(int32_t) * (size_t)(nf + 4));
   L.tiles = take(sizeof(unsigned long long) * (size_t)scan_tiles(nf));
+  L.bcur = take(sizeof(int32_t) * PART_NB);
   L.rec = take(sizeof(float4) * (size_t)cap);
   L.sid = take(sizeof(int32_t) * (size_t)cap);
   L.perm = take(sizeof(int32_t) * (size_t)cap);
   L.urec = take(sizeof(float4) * (size_t)cap);
   L.uid = take(sizeof(int32_t) * (size_t)cap);
-  L.rank = take(sizeof(int32_t) * (size_t)cap);
+  L.tidx = take(sizeof(int32_t) * (size_t)cap);
   L.outs = take(sizeof(float4) * (size_t)cap);
   L.io = take(sizeof(float) * 8 * (size_t)cap);
   L.pairs = take(sizeof(float4) * 2 * (size_t)(cap / 2 + 1));
@@ -153,7 +154,7 @@ struct pi_ctx_s {
   Layout lay;
   unsigned char *ws;
   DevCtl *ctl;
-  int32_t *counts, *offsets, *foffsets, *pcounts, *sid, *perm, *uid, *rank;
+  int32_t *counts, *offsets, *foffsets, *pcounts, *sid, *perm, *uid, *tidx, *bcur;
   unsigned long long *tiles;
   float4 *rec, *urec, *outs, *pairs;
   float *io;
@@ -274,7 +275,8 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   c->perm = reinterpret_cast<int32_t *>(c->ws + lay.perm);
   c->urec = reinterpret_cast<float4 *>(c->ws + lay.urec);
   c->uid = reinterpret_cast<int32_t *>(c->ws + lay.uid);
-  c->rank = reinterpret_cast<int32_t *>(c->ws + lay.rank);
+  c->tidx = reinterpret_cast<int32_t *>(c->ws + lay.tidx);
+  c->bcur = reinterpret_cast<int32_t *>(c->ws + lay.bcur);
   c->outs = reinterpret_cast<float4 *>(c->ws + lay.outs);
   c->io = reinterpret_cast<float *>(c->ws + lay.io);
   c->pairs = reinterpret_cast<float4 *>(c->ws + lay.pairs);
@@ -399,8 +401,9 @@ static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, c
   a.x = x; a.y = y; a.z = z; a.q = q;
   a.rec_in = rec_in;
   a.id_in = id;
-  a.cell_of = nullptr;
-  a.rank = c->rank;
+  a.tmp_rec = c->urec;  // free during pi_bin (pi_step's update buffer)
+  a.tmp_idx = c->tidx;
+  a.bucket_cur = c->bcur;
   a.counts = c->counts;
   a.offsets = c->offsets;
   a.foffsets = c->foffsets;

@@ -186,14 +186,17 @@ __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, in
 // ------------------------------------------------------------------------------------
 // Launchers (host side, in the .cu files).
 // ------------------------------------------------------------------------------------
+constexpr int PART_NB = 1024;  // max buckets of the partitioned pi_bin (2 per thread in its scan)
+
 struct BinArgs {
   long long n;                  // particles (upper bound when n_dev is set)
   const long long *n_dev;       // device-resident count (nranks > 1), or NULL
   const float *x, *y, *z, *q;   // SoA input (pi_bin), or NULL when rec_in is used
   const float4 *rec_in;         // AoS input (pi_step re-binning)
   const int32_t *id_in;         // ids (NULL -> index)
-  int32_t *cell_of;             // optional: a1 output in input order
-  int32_t *rank;                // scratch [n]
+  float4 *tmp_rec;              // SoA path scratch [n]: records partitioned into buckets
+  int32_t *tmp_idx;             // SoA path scratch [n]: their caller indices
+  int32_t *bucket_cur;          // SoA path scratch [PART_NB]: bucket fill cursors
   int32_t *counts;              // [ncells sx] fine counts, zero on entry and again after the binning
   int32_t *offsets;             // [ncells + 1] per cell
   int32_t *foffsets;            // [ncells sx + 1] per fine cell (the sorted order)
@@ -203,8 +206,8 @@ struct BinArgs {
   int32_t *sid_out;             // sorted ids
   int32_t *perm_out;            // sorted slot -> input index (nullable)
   const int32_t *perm_in;       // AoS path: input index per record (-1 = ghost), or NULL
-  float4 *pairs_out;            // AoS path, nullable: also write the sorted records as f32x2
-                                // source pairs (layout of InteractArgs::pairs)
+  float4 *pairs_out;            // AoS input, nullable: also write the sorted records as f32x2 source pairs
+                                // (layout of InteractArgs::pairs)
   int32_t *pcounts;             // [ncells sx] persistent counts of the sorted state (one rank)
   bool delta;                   // AoS re-binning from pcounts (kept current by the pi_step update)
   DevCtl *ctl;

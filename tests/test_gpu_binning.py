@@ -101,3 +101,20 @@ def test_rebinning_is_repeatable():
     ctx = ctx_for(c)
     for _ in range(3):  # counts are re-zeroed by the scan; the look-back epoch advances
         check_binning(c, ctx)
+
+
+@pytest.mark.parametrize("kind", ["clustered", "nondyadic"])
+def test_partitioned_buckets_with_ids(kind):
+    """Random-order pi_bin partitions into buckets of ~2^17 particles before the scatter: cover
+    several (uneven) buckets, a non-power-of-two cell count, a ragged tile and caller ids."""
+    n = 3 * (1 << 18) + 4101
+    if kind == "clustered":
+        cloud = synth.clustered(n, synth.Grid(dims=(64, 64, 64), w=1 / 64), seed=31)
+    else:
+        cloud = synth.uniform(n, synth.Grid(dims=(60, 44, 36), w=1 / 64), seed=32)
+    ctx = check_binning(cloud)
+    ids = np.random.default_rng(7).permutation(n).astype(np.int32) * 3 + 1
+    ctx.bin(*to_dev(cloud), torch.from_numpy(ids).cuda())
+    _, _, _, perm = ctx.get_binning()
+    parts = ctx.get_particles()
+    assert np.array_equal(parts["id"].cpu().numpy(), ids[perm.cpu().numpy()])

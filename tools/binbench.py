@@ -14,7 +14,11 @@ from paper_2406_16091_b200 import Context
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="c1,c2_ppc8,c3")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--lib", default=None, help="alternative libpi.so (A/B)")
 a = ap.parse_args()
+if a.lib:
+    import paper_2406_16091_b200._lib as L
+    L.LIBPATH = os.path.abspath(a.lib)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for name in a.configs.split(","):
     c = synth.make_config(name)
