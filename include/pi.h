@@ -139,14 +139,15 @@ typedef struct {
 
 /* Tuning knobs of the launch configuration (a5).  Zero fields mean "library default".   */
 typedef struct {
-  int32_t xpencil_len;       /* X-pencil: target cells per warp work item along X (16)      */
-  int32_t xpencil_cap;       /* X-pencil: records of one merged 9-row cell a warp stages;
-                                larger cells take the global-memory path (mean + 4.5 sd)   */
+  int32_t xpencil_len;       /* X-pencil: target cells per work item (row segment) (64)     */
+  int32_t xpencil_cap;       /* X-pencil: records one staging slot holds (9 pencils of the
+                                segment at the mean density + 15 %); a segment that does
+                                not fit is split into rounds, a cell whose window alone does
+                                not fit takes the global-memory path                        */
   int32_t fullload_box[3];   /* full load: target sub-box (interior) dims (8, 4, 4)         */
   int32_t fullload_cap;      /* full load: staged particles per block                       */
   int32_t threads;           /* threads per block of the staged kernels                     */
-  int32_t lanes_per_target;  /* X-pencil: max lanes sharing one target (1..8; default 8,
-                                used as min(8, 32 / targets in the cell))                   */
+  int32_t xpencil_slots;     /* X-pencil: staging slots per block (2..4; default 2)         */
   int32_t reserved[7];
 } pi_tuning;
 

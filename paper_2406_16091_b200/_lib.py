@@ -34,7 +34,7 @@ class pi_stats(ctypes.Structure):
 class pi_tuning(ctypes.Structure):
     _fields_ = [("xpencil_len", ctypes.c_int32), ("xpencil_cap", ctypes.c_int32),
                 ("fullload_box", ctypes.c_int32 * 3), ("fullload_cap", ctypes.c_int32), ("threads", ctypes.c_int32),
-                ("lanes_per_target", ctypes.c_int32),
+                ("xpencil_slots", ctypes.c_int32),
                 ("reserved", ctypes.c_int32 * 7)]
 
 

@@ -9,7 +9,7 @@
 //     (X-fastest linearisation), so a pencil arrives with one TMA bulk copy
 //     (cp.async.bulk, completion counted in bytes on the slot's mbarrier): 9 copies per item,
 //     issued by a single producer warp -- no per-particle staging work at all;
-//   * persistent blocks stream the items through NSLOT = 2 slots: while the consumer warps
+//   * persistent blocks stream the items through nslot (2..4) slots: while the consumer warps
 //     compute one slot the producer refills the other.  Slots are handed over with mbarriers
 //     (full: TMA bytes + producer arrival; empty: one arrival per consumer warp), consumer
 //     warps take 32-target batches from a per-slot counter and move on to the next slot as
@@ -41,7 +41,7 @@ extern "C" __attribute__((visibility("default"))) void pi_debug_xp_profile(unsig
 namespace pi {
 namespace {
 
-constexpr int NSLOT = 2;
+constexpr int MAX_SLOTS = 4;
 constexpr int META = 16;
 constexpr float DUMMY_X = 1.0e30f;  // inert partner of an odd run's last record: K = 0, q = 0
 
@@ -58,6 +58,7 @@ struct XpParams {
   int sx;            // X sub-cells per cell
   bool mask;         // mask the out-of-run halves of a run's end pairs (walk9)
   int capp;          // staged source pairs per slot
+  int nslot;         // staging slots (2..MAX_SLOTS)
   int nseg;          // segments per X row
   long long nitems;  // rows x segments
 };
@@ -73,7 +74,9 @@ __host__ __device__ inline int slot_words(int L, int sx) { return (META + 9 * lf
 __host__ __device__ inline size_t slot_bytes(int L, int capp, int sx) {
   return (size_t)capp * 32 + (size_t)slot_words(L, sx) * 4;
 }
-__host__ __device__ inline size_t xp_smem_bytes(int L, int capp, int sx) { return 128 + NSLOT * slot_bytes(L, capp, sx); }
+__host__ __device__ inline size_t xp_smem_bytes(int L, int capp, int sx, int nslot) {
+  return 128 + nslot * slot_bytes(L, capp, sx);
+}
 
 struct Slot {
   float4 *S;
@@ -227,8 +230,9 @@ __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, 
 template <int KERNEL, int NC, bool UPD>  // UPD: pi_step (update + carried counts in the epilogue)
 __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned long long *full = reinterpret_cast<unsigned long long *>(smem_raw);  // [NSLOT]
-  unsigned long long *empty = full + NSLOT;                                      // [NSLOT]
+  const int NSLOT = p.nslot;
+  unsigned long long *full = reinterpret_cast<unsigned long long *>(smem_raw);  // [nslot]
+  unsigned long long *empty = full + MAX_SLOTS;                                  // [nslot]
   unsigned char *slots = smem_raw + 128;
   const int L = p.L, sx = p.sx, LF = lf_of(L, sx);
   const Geom &g = p.g;
@@ -403,7 +407,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
 
 template <int NC>
 cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
-  const size_t smem = xp_smem_bytes(p.L, p.capp, p.sx);
+  const size_t smem = xp_smem_bytes(p.L, p.capp, p.sx, p.nslot);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(kern);
     if (e != cudaSuccess) return e;
@@ -460,9 +464,10 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
     cap = (int)(9.0 * ppc * 1.15 * (p.L + 2) + 64.0);
   }
   p.capp = max(16, cap / 2 + 9);  // + one partial pair per run
+  p.nslot = a.slots >= 2 ? min(a.slots, MAX_SLOTS) : 2;
   const size_t max_smem = 227 * 1024;
-  while (xp_smem_bytes(p.L, p.capp, p.sx) > max_smem && p.capp > 64) p.capp -= 32;
-  if (xp_smem_bytes(p.L, p.capp, p.sx) > max_smem) return cudaErrorNotSupported;
+  while (xp_smem_bytes(p.L, p.capp, p.sx, p.nslot) > max_smem && p.capp > 64) p.capp -= 32;
+  if (xp_smem_bytes(p.L, p.capp, p.sx, p.nslot) > max_smem) return cudaErrorNotSupported;
   p.pairs = a.pairs;
   if (!a.pairs_ready) {  // the AoS binning (pi_step) writes the pairs itself
     const long long np = (a.n + 1) / 2;

@@ -227,7 +227,7 @@ struct InteractArgs {
   const int32_t *foffsets;      // [ncells sx + 1] fine offsets (X sub-cells)
   OutDesc out;
   DevCtl *ctl;
-  int tx_len, tx_cap, threads, groups;  // tuning (x-pencil)
+  int tx_len, tx_cap, threads, slots;  // tuning (x-pencil)
   int fb[3], fb_cap;            // tuning (full load)
 };
 

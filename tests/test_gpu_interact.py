@@ -144,8 +144,8 @@ def test_xpencil_tuning_shapes(algo):
     want = oracle_interact(c)
     for tune in (dict(xpencil_len=1), dict(xpencil_len=7, xpencil_cap=300), dict(xpencil_len=64),
                  dict(xpencil_len=16, xpencil_cap=64), dict(threads=256, xpencil_len=5), dict(threads=32),
-                 dict(xpencil_cap=16), dict(lanes_per_target=1), dict(lanes_per_target=3),
-                 dict(lanes_per_target=4, threads=256), dict(lanes_per_target=4)):
+                 dict(xpencil_cap=16), dict(xpencil_slots=3), dict(xpencil_slots=4, xpencil_len=16),
+                 dict(xpencil_slots=4, threads=256), dict(xpencil_slots=5)):
         got, ctx = gpu_interact(c, algo, tuning=tune)
         assert_parity(got, want, label=f"{algo} {tune}")
         if algo == "xpencil" and tune.get("xpencil_cap") in (16, 64):
