@@ -75,7 +75,7 @@ __host__ __device__ inline size_t slot_bytes(int L, int capp, int sx) {
   return (size_t)capp * 32 + (size_t)slot_words(L, sx) * 4;
 }
 __host__ __device__ inline size_t xp_smem_bytes(int L, int capp, int sx, int nslot) {
-  return 128 + nslot * slot_bytes(L, capp, sx);
+  return 128 + nslot * slot_bytes(L, capp, sx) + (size_t)9 * lf_of(L, sx) * 4;  // + offsets staging
 }
 
 struct Slot {
@@ -111,36 +111,47 @@ __global__ void k_pairify(long long n, const long long *n_dev, const float4 *__r
 }
 
 // ---------------------------------------------------------------- producer (one warp)
+// The producer's next item: its offset tables are fetched with cp.async into a staging
+// table while the current item is computed, then copied into the slot (the global-load
+// latency is otherwise on the critical path of every slot refill: measured, consumers found
+// a third of the slots not yet filled).
+__device__ __forceinline__ void item_geom(const XpParams &p, long long item, int &x0, int &Lseg, int &cy, int &cz) {
+  const int seg = (int)(item % p.nseg);
+  const long long row = item / p.nseg;
+  cy = (int)(row % p.g.ny);
+  cz = (int)(row / p.g.ny);
+  x0 = p.g.own_lo + seg * p.L;
+  Lseg = min(p.L, p.g.own_hi - x0);
+}
+__device__ __forceinline__ void cp_async4(int *dst, const int *src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
 // Fine offsets of the 9 pencils of `item` at the X sub-cell boundaries of cells x0-1 .. x0+L
-// (clamped: cells outside the grid are empty).
-__device__ void load_offsets(const XpParams &p, const Slot &sl, long long item, int &x0, int &Lseg, int &cy,
-                             int &cz) {
+// (clamped: rows outside the grid are empty) -> stage[9][LF], asynchronously.
+__device__ __forceinline__ void prefetch_offsets(const XpParams &p, long long item, int *stage) {
   const int lane = threadIdx.x & 31;
   const int LF = lf_of(p.L, p.sx), sx = p.sx;
   const Geom &g = p.g;
-  const int seg = (int)(item % p.nseg);
-  const long long row = item / p.nseg;
-  cy = (int)(row % g.ny);
-  cz = (int)(row / g.ny);
-  x0 = g.own_lo + seg * p.L;  // owned X cells only (ghost layers are staged as sources)
-  Lseg = min(p.L, g.own_hi - x0);
+  int x0, Lseg, cy, cz;
+  item_geom(p, item, x0, Lseg, cy, cz);
   const int nxf = g.nx * sx;
-  for (int k0 = 0; k0 < LF; k0 += 32) {
-    const int k = k0 + lane;
+  for (int k = lane; k < LF; k += 32) {
     const int bf = min(max((x0 - 1) * sx + k, 0), nxf);
-    int v[9];
 #pragma unroll
     for (int r = 0; r < 9; ++r) {
       const int y = cy + (r % 3) - 1, z = cz + (r / 3) - 1;
-      v[r] = 0;
-      if (k < LF && y >= 0 && y < g.ny && z >= 0 && z < g.nz)
-        v[r] = __ldg(p.foffsets + (long long)nxf * (y + (long long)g.ny * z) + bf);
-    }
-    if (k < LF) {
-#pragma unroll
-      for (int r = 0; r < 9; ++r) sl.O[r * LF + k] = v[r];
+      const bool ok = y >= 0 && y < g.ny && z >= 0 && z < g.nz;
+      cp_async4(stage + r * LF + k, p.foffsets + (ok ? (long long)nxf * (y + (long long)g.ny * z) + bf : 0), ok);
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void take_offsets(const XpParams &p, const Slot &sl, const int *stage) {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+  const int n = 9 * lf_of(p.L, p.sx);
+  for (int k = threadIdx.x & 31; k < n; k += 32) sl.O[k] = stage[k];
   __syncwarp();
 }
 
@@ -250,8 +261,12 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
 
   if (warp == NC) {
     // ================================ producer ================================
-    long long item = -1;
+    long long item = -1, next = 0;
     int x0 = 0, Lseg = 0, cy = 0, cz = 0, ja = 1;
+    int *stage = reinterpret_cast<int *>(slots + (size_t)NSLOT * slot_bytes(L, p.capp, sx));
+    if (lane == 0) next = (long long)atomicAdd(&p.ctl->xp_items, 1ull);
+    next = __shfl_sync(0xffffffffu, next, 0);
+    if (next < p.nitems) prefetch_offsets(p, next, stage);
     for (unsigned use = 0;; ++use) {
       const int s = use % NSLOT;
       const Slot sl = slot_at(slots, L, p.capp, sx, s);
@@ -260,9 +275,9 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       XP_T(t1);
       XP_ADD(0, t0, t1);
       fence_proxy_async();  // their generic reads of the slot precede the TMA writes below
-      if (item < 0 || ja > Lseg) {
-        if (lane == 0) item = (long long)atomicAdd(&p.ctl->xp_items, 1ull);
-        item = __shfl_sync(0xffffffffu, item, 0);
+      const bool fresh = item < 0 || ja > Lseg;
+      if (fresh) {
+        item = next;
         if (item >= p.nitems) {  // stop marker: consumers leave at the first one
           if (lane == 0) {
             sl.meta[0] = 1;
@@ -270,7 +285,8 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
           }
           break;
         }
-        load_offsets(p, sl, item, x0, Lseg, cy, cz);
+        item_geom(p, item, x0, Lseg, cy, cz);
+        take_offsets(p, sl, stage);
         ja = 1;
       } else {
         // next round of the same item: the offsets are reused (copy them into this slot)
@@ -309,6 +325,11 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       __syncwarp();
       if (lane < 9 && len > 0) bulk_g2s(sl.S + 2 * (incl - len), p.pairs + 2 * (long long)a, (unsigned)len * 32u, &full[s]);
       ja = last + 1;
+      if (fresh) {  // the slot is on its way: fetch the following item's offsets meanwhile
+        if (lane == 0) next = (long long)atomicAdd(&p.ctl->xp_items, 1ull);
+        next = __shfl_sync(0xffffffffu, next, 0);
+        if (next < p.nitems) prefetch_offsets(p, next, stage);
+      }
       XP_T(t2);
       XP_ADD(1, t1, t2);
       XP_ADD(2, 0, 1);
