@@ -166,7 +166,7 @@ def workload_config(a, world, cloud, n_total):
     else:
         workload = f"synth.make_config({a.config!r}): {cloud.n} particles, {tuple(g.dims)} cells, Gaussian K, fp32"
     return {"workload": workload, "n_per_gpu": cloud.n, "n_total": int(n_total), "cells": g.ncells,
-            "algo": a.algo, "step": "pi_step: bin (count+scan+scatter) + interact + integrate"
+            "algo": a.algo, "step": "pi_step: re-bin (scan of the carried counts + scatter) + interact + integrate"
             + (" + a8 migration/ghost exchange (NCCL)" if world > 1 else ""),
             "l2": "flushed between timed steps (256 MiB write, outside the events)",
             "parallelism": f"xslab{world}" if world > 1 else "single GPU"}

@@ -72,7 +72,7 @@ for name, title in (("xpencil", "X-pencil interaction (configs[1], 2^21, 64^3)")
         s, tr = fmt(d)
         out.append(f"## {title}: `{d['Kernel Name'][:60]}`\n{s}\n")
         traffic[name] = int(tr)
-for name, title in (("rebin", "binning, pi_step re-binning at 2^24 (configs[2] ppc 8, nearly sorted AoS input)"),
+for name, title in (("rebin", "binning, pi_step delta re-binning at 2^24 (configs[2] ppc 8: scan of the carried counts + scatter of the nearly sorted records)"),
                     ("bin", "binning, pi_bin at 2^24 (configs[2] ppc 8, random input order)")):
     rep = os.path.join(G, f"{R}_{name}.ncu-rep")
     if not os.path.exists(rep):
@@ -94,7 +94,7 @@ if os.path.exists(ll):
         tot[k] += float(r[iV])
         cnt[k] += 1
     s = sum(tot.values())
-    out.append("## Launch list of `bench.py --steps 3 --warmup 3` (all kernels of the run, ncu-serialised)\n")
+    out.append("## Launch list of `bench.py --steps 3 --warmup 3 --no-binning-2e24` (all kernels of the run, ncu-serialised)\n")
     out.append("| kernel | launches | total us | share |\n|---|---|---|---|")
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
         out.append(f"| `{k}` | {cnt[k]} | {v / 1e3:.1f} | {100 * v / s:.1f} % |")
