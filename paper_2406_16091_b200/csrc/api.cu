@@ -82,7 +82,7 @@ Layout make_layout(const pi_config *cfg) {
   L.tidx = take(sizeof(int32_t) * (size_t)cap);
   L.outs = take(sizeof(float4) * (size_t)cap);
   L.io = take(sizeof(float) * 8 * (size_t)cap);
-  L.pairs = take(sizeof(float4) * 2 * (size_t)(cap / 2 + 1));
+  L.pairs = take(sizeof(float4) * 2 * (size_t)pair_plane_of(cap));  // two planes (A: x, y; B: z, q)
   if (cfg->nranks > 1) {
     L.xrec = take(sizeof(float4) * (size_t)cap);
     L.xid = take(sizeof(int32_t) * (size_t)cap);
@@ -414,6 +414,7 @@ static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, c
   a.perm_out = (rec_in && !perm_in) ? nullptr : c->perm;
   a.perm_in = perm_in;
   a.pairs_out = rec_in ? c->pairs : nullptr;
+  a.pair_plane = pair_plane_of(c->cfg.capacity);
   c->pairs_ready = rec_in != nullptr;
   a.ctl = c->ctl;
   phase_begin(c, 0);
@@ -476,6 +477,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.rec = c->rec_ok ? c->rec : nullptr;
   a.foffsets = c->foffsets;
   a.pairs = c->pairs;
+  a.pair_plane = pair_plane_of(c->cfg.capacity);
   a.pairs_ready = c->pairs_ready;
   a.offsets = c->offsets;
   a.ctl = c->ctl;

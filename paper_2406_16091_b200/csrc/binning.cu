@@ -399,7 +399,8 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
                                                             int32_t *__restrict__ perm_out,
                                                             const int32_t *__restrict__ perm_in,
                                                             const long long *n_dev,
-                                                            float *__restrict__ pairs_out = nullptr) {
+                                                            float *__restrict__ pairs_out = nullptr,
+                                                            long long plane = 0) {
   if (n_dev) n = *n_dev;
   for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
     const long long i = i0 + threadIdx.x;
@@ -411,17 +412,18 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
     if (!ok) continue;
     int slot = __ldg(offsets + lin) + rk;  // fine offsets
     if (rec_out) rec_out[slot] = r;       // (pi_step with the X-pencil: the pair array only)
-    if (pairs_out) {  // f32x2 source-pair layout: P[2k] = (x0, x1, y0, y1), P[2k+1] = (z0, z1, q0, q1)
-      float *pp = pairs_out + 8 * (long long)(slot >> 1) + (slot & 1);
-      pp[0] = r.x;
-      pp[2] = r.y;
-      pp[4] = r.z;
-      pp[6] = r.w;
+    if (pairs_out) {  // f32x2 source pairs: A[k] = (x0, x1, y0, y1), B[k] = (z0, z1, q0, q1), B = A + plane
+      float *pa = pairs_out + 4 * (long long)(slot >> 1) + (slot & 1);
+      float *pb = pa + 4 * plane;
+      pa[0] = r.x;
+      pa[2] = r.y;
+      pb[0] = r.z;
+      pb[2] = r.w;
       if (slot == n - 1 && !(slot & 1)) {  // odd count: an inert partner for the last record
-        pp[1] = 1.0e30f;
-        pp[3] = 1.0e30f;
-        pp[5] = 1.0e30f;
-        pp[7] = 0.f;
+        pa[1] = 1.0e30f;
+        pa[3] = 1.0e30f;
+        pb[1] = 1.0e30f;
+        pb[3] = 0.f;
       }
     }
     if (GATHER) {
@@ -457,7 +459,8 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
                                                 a.offsets, a.counts);
     if (a.n > 0)
       k_scatter<false><<<sgrid, COUNT_THREADS, 0, s>>>(a.n, a.rec_in, a.id_in, g, a.counts, a.foffsets, a.rec_out,
-                                                       a.sid_out, a.perm_out, a.perm_in, a.n_dev, pairs);
+                                                       a.sid_out, a.perm_out, a.perm_in, a.n_dev, pairs,
+                                                       a.pair_plane);
     return cudaGetLastError();
   }
   if (a.rec_in) {  // AoS: count, scan keeping the counts, scatter taking ranks from them
@@ -467,7 +470,8 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
                                                 a.offsets, a.pcounts);
     if (a.n > 0)
       k_scatter<false><<<sgrid, COUNT_THREADS, 0, s>>>(a.n, a.rec_in, a.id_in, g, a.counts, a.foffsets, a.rec_out,
-                                                       a.sid_out, a.perm_out, a.perm_in, a.n_dev, pairs);
+                                                       a.sid_out, a.perm_out, a.perm_in, a.n_dev, pairs,
+                                                       a.pair_plane);
     return cudaGetLastError();
   }
   // SoA (pi_bin, arbitrary order): count, scan keeping the counts, partition into buckets of

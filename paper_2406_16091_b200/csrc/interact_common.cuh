@@ -94,15 +94,18 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Staged sources are stored as PAIRS (sources 2p and 2p+1) in two 16-B halves:
-//   S[2p]   = (x~_2p, x~_2p+1, y~_2p, y~_2p+1)      S[2p+1] = (z~_2p, z~_2p+1, q_2p, q_2p+1)
+// Staged sources are stored as PAIRS (sources 2p and 2p+1) in two planes of 16-B elements:
+//   A[p] = (x~_2p, x~_2p+1, y~_2p, y~_2p+1)      B[p] = (z~_2p, z~_2p+1, q_2p, q_2p+1)
 // so one LDS.128 yields aligned f32x2 operands and the lane's scalar target coordinate is
-// the broadcast operand of FADD2 (FADD2 R, R.F32x2, -Rt.F32).
+// the broadcast operand of FADD2 (FADD2 R, R.F32x2, -Rt.F32).  Planes rather than the
+// interleaved A[p] B[p] records: the lanes of a quarter-warp read pairs a few apart (targets in
+// neighbouring X sub-cells), which conflict when p == p' mod 8 on planes but p == p' mod 4 when
+// interleaved (measured: 4.27 wavefronts per LDS.128 interleaved against 3.3 ideal).
 struct SrcPair {
   p2 x, y, z, q;
 };
-__device__ __forceinline__ SrcPair load_pair(const float4 *__restrict__ S, int p) {
-  const float4 a = S[2 * p], b = S[2 * p + 1];
+__device__ __forceinline__ SrcPair load_pair(const float4 *__restrict__ A, const float4 *__restrict__ B, int p) {
+  const float4 a = A[p], b = B[p];
   SrcPair r;
   r.x = pk(a.x, a.y);
   r.y = pk(a.z, a.w);
@@ -199,11 +202,11 @@ __device__ __forceinline__ void scalar_term(const KParams &kp, float r2, float q
 // Fallback for a target whose cell window does not fit the staging buffer: Par-Part-NoLoop
 // over global memory (Alg. 1) for target slot t in cell (cx, cy, cz).
 // Record s of the sorted state: from the records, or (rec == NULL) from the f32x2 pair array
-// P[2k] = (x_2k, x_2k+1, y_2k, y_2k+1), P[2k+1] = (z.., z.., q.., q..).
+// A[k] = (x_2k, x_2k+1, y_2k, y_2k+1) = pairs[k], B[k] = (z.., z.., q.., q..) = pairs[plane + k].
 __device__ __forceinline__ float4 sorted_rec(const float4 *__restrict__ rec, const float4 *__restrict__ pairs,
-                                             int s) {
+                                             long long plane, int s) {
   if (rec) return __ldg(rec + s);
-  const float4 a = __ldg(pairs + 2 * (s >> 1)), b = __ldg(pairs + 2 * (s >> 1) + 1);
+  const float4 a = __ldg(pairs + (s >> 1)), b = __ldg(pairs + plane + (s >> 1));
   return (s & 1) ? make_float4(a.y, a.w, b.y, b.w) : make_float4(a.x, a.z, b.x, b.z);
 }
 
@@ -211,9 +214,9 @@ template <int KERNEL, bool UPD = true>
 __device__ void fallback_target(int t, int cx, int cy, int cz, const float4 *__restrict__ rec,
                                 const int32_t *__restrict__ offsets, const Geom &g, const KParams &kp,
                                 const OutDesc &out, unsigned long long &cand,
-                                const float4 *__restrict__ pairs = nullptr) {
+                                const float4 *__restrict__ pairs = nullptr, long long plane = 0) {
   const int xlo = max(cx - 1, 0), xhi = min(cx + 1, g.nx - 1);
-  const float4 me = sorted_rec(rec, pairs, t);
+  const float4 me = sorted_rec(rec, pairs, plane, t);
   float phi = 0.f, fx = 0.f, fy = 0.f, fz = 0.f;
   for (int dz = -1; dz <= 1; ++dz) {
     const int z = cz + dz;
@@ -226,7 +229,7 @@ __device__ void fallback_target(int t, int cx, int cy, int cz, const float4 *__r
       cand += (unsigned long long)(hi_ - lo_);
       for (int s = lo_; s < hi_; ++s) {
         if (s == t) continue;
-        const float4 o = sorted_rec(rec, pairs, s);
+        const float4 o = sorted_rec(rec, pairs, plane, s);
         const float dx = me.x - o.x, dy2 = me.y - o.y, dz2 = me.z - o.z;
         const float r2 = fmaf(dz2, dz2, fmaf(dy2, dy2, dx * dx));
         if (KERNEL == PI_K_CANDIDATE) {

@@ -47,7 +47,8 @@ constexpr float DUMMY_X = 1.0e30f;  // inert partner of an odd run's last record
 
 struct XpParams {
   const float4 *rec;
-  const float4 *pairs;  // the sorted records as f32x2 source pairs (k_pairify)
+  const float4 *pairs;  // the sorted records as f32x2 source pairs (k_pairify): planes A | B
+  long long plane;      // float4 elements per plane
   const int32_t *offsets;
   const int32_t *foffsets;  // fine offsets: sx X sub-cells per cell (the sorted order)
   Geom g;
@@ -63,7 +64,8 @@ struct XpParams {
   long long nitems;  // rows x segments
 };
 
-// Slot: S[2 capp] float4 (source pairs) | meta[16] | O[9][LF] | rb[16],  LF = (L+2) sx + 1
+// Slot: SA[capp] | SB[capp] float4 (source pairs, planes A and B) | meta[16] | O[9][LF] | rb[16],
+// LF = (L+2) sx + 1
 //   O[r][k]  global offsets of pencil r (= (dy + 1) + 3 (dz + 1)) at the fine (X sub-cell)
 //            boundary k of the cells x0-1 .. x0+L; the cell boundary j is O[r][j sx]
 //   rb[r]    first staged pair of pencil r's run in S (rb[9] = total)
@@ -79,13 +81,14 @@ __host__ __device__ inline size_t xp_smem_bytes(int L, int capp, int sx, int nsl
 }
 
 struct Slot {
-  float4 *S;
+  float4 *S, *SB;  // planes A (x, y) and B (z, q) of the staged source pairs
   int *meta, *O, *rb;
 };
 __device__ __forceinline__ Slot slot_at(unsigned char *base, int L, int capp, int sx, int s) {
   unsigned char *u = base + (size_t)s * slot_bytes(L, capp, sx);
   Slot sl;
   sl.S = reinterpret_cast<float4 *>(u);
+  sl.SB = sl.S + capp;
   sl.meta = reinterpret_cast<int *>(u + (size_t)capp * 32);
   sl.O = sl.meta + META;
   sl.rb = sl.O + 9 * lf_of(L, sx);
@@ -96,17 +99,18 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// The cell-sorted records as source pairs P[2k] = (x_2k, x_2k+1, y_2k, y_2k+1),
-// P[2k+1] = (z_2k, z_2k+1, q_2k, q_2k+1) (bitwise copies; an odd count gets an inert partner),
-// so that a pencil run is staged by TMA already in the layout the f32x2 inner loop reads.
-__global__ void k_pairify(long long n, const long long *n_dev, const float4 *__restrict__ rec, float4 *P) {
+// The cell-sorted records as source pairs A[k] = P[k] = (x_2k, x_2k+1, y_2k, y_2k+1),
+// B[k] = P[plane + k] = (z_2k, z_2k+1, q_2k, q_2k+1) (bitwise copies; an odd count gets an inert
+// partner), so that a pencil run is staged by TMA already in the layout the f32x2 loop reads.
+__global__ void k_pairify(long long n, const long long *n_dev, const float4 *__restrict__ rec, float4 *P,
+                          long long plane) {
   if (n_dev) n = *n_dev;
   const long long np = (n + 1) >> 1;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < np; k += (long long)gridDim.x * blockDim.x) {
     const float4 a = rec[2 * k];
     const float4 b = 2 * k + 1 < n ? rec[2 * k + 1] : make_float4(DUMMY_X, DUMMY_X, DUMMY_X, 0.f);
-    P[2 * k] = make_float4(a.x, b.x, a.y, b.y);
-    P[2 * k + 1] = make_float4(a.z, b.z, a.w, b.w);
+    P[k] = make_float4(a.x, b.x, a.y, b.y);
+    P[plane + k] = make_float4(a.z, b.z, a.w, b.w);
   }
 }
 
@@ -192,6 +196,7 @@ template <int KERNEL, bool MASK>
 __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, int klo, int khi, const float4 me,
                                         const float thr, const float mc2, const KParams &kp) {
   const float4 *__restrict__ S = sl.S;
+  const float4 *__restrict__ SB = sl.SB;
   p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
   p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
 #pragma unroll  // the 9 runs unrolled: their bounds loads schedule early (measured: -1 %)
@@ -203,27 +208,27 @@ __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, 
     if (!MASK) {
       int q = p0;
       for (; q + 1 <= pl; q += 2) {
-        const SrcPair s0 = load_pair(S, q), s1 = load_pair(S, q + 1);
+        const SrcPair s0 = load_pair(S, SB, q), s1 = load_pair(S, SB, q + 1);
         src_eval<KERNEL>(s0, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
         src_eval<KERNEL>(s1, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
       }
-      if (q <= pl) src_eval<KERNEL>(load_pair(S, q), me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
+      if (q <= pl) src_eval<KERNEL>(load_pair(S, SB, q), me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
       continue;
     }
     {
-      SrcPair f = load_pair(S, p0);
+      SrcPair f = load_pair(S, SB, p0);
       f.q = pk((a & 1) ? 0.f : lo(f.q), (p0 == pl && (b & 1)) ? 0.f : hi(f.q));
       src_eval<KERNEL>(f, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
     }
     if (pl > p0) {
       int q = p0 + 1;
       for (; q + 2 <= pl; q += 2) {
-        const SrcPair s0 = load_pair(S, q), s1 = load_pair(S, q + 1);
+        const SrcPair s0 = load_pair(S, SB, q), s1 = load_pair(S, SB, q + 1);
         src_eval<KERNEL>(s0, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
         src_eval<KERNEL>(s1, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
       }
-      if (q < pl) src_eval<KERNEL>(load_pair(S, q), me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
-      SrcPair l = load_pair(S, pl);
+      if (q < pl) src_eval<KERNEL>(load_pair(S, SB, q), me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
+      SrcPair l = load_pair(S, SB, pl);
       l.q = pk(lo(l.q), (b & 1) ? 0.f : hi(l.q));
       src_eval<KERNEL>(l, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
     }
@@ -323,7 +328,10 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&full[s], (unsigned)total * 32u);  // release: tables
       __syncwarp();
-      if (lane < 9 && len > 0) bulk_g2s(sl.S + 2 * (incl - len), p.pairs + 2 * (long long)a, (unsigned)len * 32u, &full[s]);
+      if (lane < 9 && len > 0) {
+        bulk_g2s(sl.S + (incl - len), p.pairs + a, (unsigned)len * 16u, &full[s]);
+        bulk_g2s(sl.SB + (incl - len), p.pairs + p.plane + a, (unsigned)len * 16u, &full[s]);
+      }
       ja = last + 1;
       if (fresh) {  // the slot is on its way: fetch the following item's offsets meanwhile
         if (lane == 0) next = (long long)atomicAdd(&p.ctl->xp_items, 1ull);
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         if (T < ntargets) {
           const int gs = t0 + T;
           if (jb < ja) {  // fallback round: cell ja from global memory
-            fallback_target<KERNEL, UPD>(gs, x0 - 1 + ja, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand, p.pairs);
+            fallback_target<KERNEL, UPD>(gs, x0 - 1 + ja, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand, p.pairs, p.plane);
             if (T == 0) ++fallbacks;
           } else {
             // cell of the target: last j in [ja, jb] with O4[j sx] <= gs
@@ -372,7 +380,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
             }
             const int j = lo_;
             const int tp = sl.rb[4] - (O4[(ja - 1) * sx] >> 1) + (gs >> 1);  // the target's pair
-            const float4 ua = sl.S[2 * tp], ub = sl.S[2 * tp + 1];
+            const float4 ua = sl.S[tp], ub = sl.SB[tp];
             const float4 me = (gs & 1) ? make_float4(ua.y, ua.w, ub.y, ub.w) : make_float4(ua.x, ua.z, ub.x, ub.z);
             // X sub-cells that can hold a source with |x_s - x_t| < r_c: the fine index is
             // monotone in x, and x_t - r_c / x_t + r_c are rounded outward, so every skipped
@@ -490,10 +498,11 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   while (xp_smem_bytes(p.L, p.capp, p.sx, p.nslot) > max_smem && p.capp > 64) p.capp -= 32;
   if (xp_smem_bytes(p.L, p.capp, p.sx, p.nslot) > max_smem) return cudaErrorNotSupported;
   p.pairs = a.pairs;
+  p.plane = a.pair_plane;
   if (!a.pairs_ready) {  // the AoS binning (pi_step) writes the pairs itself
     const long long np = (a.n + 1) / 2;
     int blocks = (int)min((np + 255) / 256, 148LL * 16);
-    k_pairify<<<max(blocks, 1), 256, 0, s>>>(a.n, a.n_dev, a.rec, a.pairs);
+    k_pairify<<<max(blocks, 1), 256, 0, s>>>(a.n, a.n_dev, a.rec, a.pairs, a.pair_plane);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -188,6 +188,13 @@ __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, in
 // ------------------------------------------------------------------------------------
 constexpr int PART_NB = 1024;  // max buckets of the partitioned pi_bin (2 per thread in its scan)
 
+// float4 elements per plane of the f32x2 source-pair array of a context of `cap` particles
+// (plane A = (x, x, y, y), plane B = (z, z, q, q) of source pairs; 128-B aligned planes)
+__host__ __device__ inline long long pair_plane_of(long long cap) {
+  if (cap < 1) cap = 1;
+  return ((cap / 2 + 1) + 7) & ~7LL;
+}
+
 struct BinArgs {
   long long n;                  // particles (upper bound when n_dev is set)
   const long long *n_dev;       // device-resident count (nranks > 1), or NULL
@@ -208,6 +215,7 @@ struct BinArgs {
   const int32_t *perm_in;       // AoS path: input index per record (-1 = ghost), or NULL
   float4 *pairs_out;            // AoS input, nullable: also write the sorted records as f32x2 source pairs
                                 // (layout of InteractArgs::pairs)
+  long long pair_plane;         // float4 elements per plane of the pair array
   int32_t *pcounts;             // [ncells sx] persistent counts of the sorted state (one rank)
   bool delta;                   // AoS re-binning from pcounts (kept current by the pi_step update)
   DevCtl *ctl;
@@ -221,7 +229,10 @@ struct InteractArgs {
   const long long *n_dev;       // device-resident count (nranks > 1), or NULL
   long long n_est;              // host estimate of the sorted count (sizes staging buffers)
   const float4 *rec;            // sorted records (NULL when only the pair array is current)
-  float4 *pairs;                // [2 * (n / 2 + 1)]: the records as f32x2 source pairs
+  float4 *pairs;                // two planes of pair_plane float4 each: the records as f32x2 source
+                                // pairs, A[k] = (x_2k, x_2k+1, y_2k, y_2k+1), B[k] = (z.., z.., q.., q..)
+                                // at pairs[k] and pairs[pair_plane + k]
+  long long pair_plane;         // >= n / 2 + 1
   bool pairs_ready;             // pairs already hold the current sorted state (AoS binning)
   const int32_t *offsets;       // [ncells + 1]
   const int32_t *foffsets;      // [ncells sx + 1] fine offsets (X sub-cells)

@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(NT) k(float *out, int reps, int wpairs, long l
     const float xt = S[2 * p0].x, yt = S[2 * p0].z, zt = S[2 * p0 + 1].x;
     p2 ph = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
     for (int q = p0; q < p0 + wpairs; ++q)
-      src_eval<PI_K_GAUSSIAN>(load_pair(S, q), xt, yt, zt, 2.4e-4f, -6.5f / 2.4e-4f, ph, fx, fy, fz);
+      src_eval<PI_K_GAUSSIAN>(load_pair(S, S + npairs, q), xt, yt, zt, 2.4e-4f, -6.5f / 2.4e-4f, ph, fx, fy, fz);
     acc += lo(ph) + hi(fx) + lo(fy) + hi(fz);
   }
   long long t1 = clock64();
