@@ -148,7 +148,10 @@ typedef struct {
   int32_t fullload_cap;      /* full load: staged particles per block                       */
   int32_t threads;           /* threads per block of the staged kernels                     */
   int32_t xpencil_slots;     /* X-pencil: staging slots per block (2..4; default 2)         */
-  int32_t reserved[7];
+  int32_t xpencil_targets;   /* X-pencil: targets per consumer lane, 1 or 2 (default 1; 2
+                                reads each staged source once for two consecutive targets;
+                                the CANDIDATE test kernel always walks one)                 */
+  int32_t reserved[6];
 } pi_tuning;
 
 PI_API int32_t pi_abi_version(void);

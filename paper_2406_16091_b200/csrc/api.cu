@@ -493,6 +493,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.tx_cap = c->tune.xpencil_cap;
   a.threads = c->tune.threads;
   a.slots = c->tune.xpencil_slots;
+  a.tpl = c->tune.xpencil_targets;
   a.fb[0] = c->tune.fullload_box[0]; a.fb[1] = c->tune.fullload_box[1]; a.fb[2] = c->tune.fullload_box[2];
   a.fb_cap = c->tune.fullload_cap;
   cudaError_t e = cudaMemsetAsync(&c->ctl->fallback_cells, 0,

@@ -60,6 +60,7 @@ struct XpParams {
   bool mask;         // mask the out-of-run halves of a run's end pairs (walk9)
   int capp;          // staged source pairs per slot
   int nslot;         // staging slots (2..MAX_SLOTS)
+  int tpl;           // targets per consumer lane (1 or 2)
   int nseg;          // segments per X row
   long long nitems;  // rows x segments
 };
@@ -243,7 +244,51 @@ __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, 
                      lo(fz) + hi(fz));
 }
 
-template <int KERNEL, int NC, bool UPD>  // UPD: pi_step (update + carried counts in the epilogue)
+// Two targets per lane (the register blocking of the paper's X-pencil-reg idea, PAPER.md
+// :421-457 §5.3: targets held in registers, every staged source read once for several of them):
+// each staged pair is loaded once for both targets, so the lane reads 8 B of shared memory per
+// candidate instead of 16 -- shared-memory wavefronts, not the FP32 pipe, bound walk9 (ncu: 81 %
+// of the LSU wavefront peak).  The window is the union [klo, khi] of the two targets' windows;
+// a source of the union outside a target's own window has |dx| >= r_c (the fine index is
+// monotone in x), so, for the cutoff kernels, it adds exactly 0, as do the out-of-run halves of
+// the end pairs (walk9, MASK = false).
+template <int KERNEL>
+__device__ __forceinline__ void walk9x2(const Slot &sl, int LF, int sx, int ja, int klo, int khi, const float4 me0,
+                                        const float4 me1, const float thr, const float mc2, const KParams &kp,
+                                        float4 &r0, float4 &r1) {
+  const float4 *__restrict__ S = sl.S;
+  const float4 *__restrict__ SB = sl.SB;
+  p2 ph0 = pk(0.f), fx0 = pk(0.f), fy0 = pk(0.f), fz0 = pk(0.f);
+  p2 ph1 = pk(0.f), fx1 = pk(0.f), fy1 = pk(0.f), fz1 = pk(0.f);
+#pragma unroll
+  for (int r = 0; r < 9; ++r) {
+    const int a = sl.O[r * LF + klo], b = sl.O[r * LF + khi + 1];
+    if (b <= a) continue;
+    const int base = sl.rb[r] - (sl.O[r * LF + (ja - 1) * sx] >> 1);
+    const int p0 = base + (a >> 1), pl = base + ((b - 1) >> 1);  // first and last pair
+    int q = p0;
+    for (; q + 1 <= pl; q += 2) {
+      const SrcPair s0 = load_pair(S, SB, q), s1 = load_pair(S, SB, q + 1);
+      src_eval<KERNEL>(s0, me0.x, me0.y, me0.z, thr, mc2, ph0, fx0, fy0, fz0, &kp);
+      src_eval<KERNEL>(s0, me1.x, me1.y, me1.z, thr, mc2, ph1, fx1, fy1, fz1, &kp);
+      src_eval<KERNEL>(s1, me0.x, me0.y, me0.z, thr, mc2, ph0, fx0, fy0, fz0, &kp);
+      src_eval<KERNEL>(s1, me1.x, me1.y, me1.z, thr, mc2, ph1, fx1, fy1, fz1, &kp);
+    }
+    if (q <= pl) {
+      const SrcPair s0 = load_pair(S, SB, q);
+      src_eval<KERNEL>(s0, me0.x, me0.y, me0.z, thr, mc2, ph0, fx0, fy0, fz0, &kp);
+      src_eval<KERNEL>(s0, me1.x, me1.y, me1.z, thr, mc2, ph1, fx1, fy1, fz1, &kp);
+    }
+  }
+  // identity exclusion (Alg. 1 :127): each target's own self pair was evaluated in the window
+  r0 = make_float4(lo(ph0) + hi(ph0) - self_term<KERNEL>(me0.w, kp), lo(fx0) + hi(fx0), lo(fy0) + hi(fy0),
+                   lo(fz0) + hi(fz0));
+  r1 = make_float4(lo(ph1) + hi(ph1) - self_term<KERNEL>(me1.w, kp), lo(fx1) + hi(fx1), lo(fy1) + hi(fy1),
+                   lo(fz1) + hi(fz1));
+}
+
+// UPD: pi_step (update + carried counts in the epilogue); TPL: targets per lane (1: walk9, 2: walk9x2)
+template <int KERNEL, int NC, bool UPD, int TPL>
 __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int NSLOT = p.nslot;
@@ -360,57 +405,81 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       // global fine X index of the item's cell 0 (fine boundaries of the tables start there)
       const int f0 = (x0 - 1 + g.gx_off) * sx;
       const float rc = p.kp.rc;
+      // target setup: its cell j (last j in [ja, jb] with O4[j sx] <= gs), its record (from the
+      // staged home pencil) and its X sub-cell window [klo, khi] (reading R18: the fine index is
+      // monotone in x and x_t -/+ r_c are rounded outward, so every skipped source has
+      // |dx| >= r_c exactly; the CANDIDATE test kernel counts every candidate: no pruning)
+      auto setup = [&](int gs, int &j, float4 &me, int &klo, int &khi) {
+        int lo_ = ja, hi_ = jb;
+        while (lo_ < hi_) {
+          const int mid = (lo_ + hi_ + 1) >> 1;
+          if (O4[mid * sx] <= gs) lo_ = mid; else hi_ = mid - 1;
+        }
+        j = lo_;
+        const int tp = sl.rb[4] - (O4[(ja - 1) * sx] >> 1) + (gs >> 1);  // the target's pair
+        const float4 ua = sl.S[tp], ub = sl.SB[tp];
+        me = (gs & 1) ? make_float4(ua.y, ua.w, ub.y, ub.w) : make_float4(ua.x, ua.z, ub.x, ub.z);
+        bool bad = false;
+        const int flo = fine_x_global(g, __fsub_rd(me.x, rc), bad) - f0;
+        const int fhi = fine_x_global(g, __fadd_ru(me.x, rc), bad) - f0;
+        klo = KERNEL == PI_K_CANDIDATE ? (j - 1) * sx : min(max(flo, (j - 1) * sx), (j + 2) * sx - 1);
+        khi = KERNEL == PI_K_CANDIDATE ? (j + 2) * sx - 1 : min(max(fhi, (j - 1) * sx), (j + 2) * sx - 1);
+      };
+      // epilogue: the 27-cell candidate count (the unit of the metric, R4, pruned or not), the
+      // target's fine cell (moves of the update are counted against it without recomputing it
+      // from the position), the output
+      auto finish = [&](int gs, int j, const float4 &me, const float4 &r) {
+        int fold = -1;
+        if (UPD && p.out.pcounts) {
+          int sub = 0;
+          while (sub + 1 < sx && O4[j * sx + sub + 1] <= gs) ++sub;
+          fold = ((x0 - 1 + j) * sx + sub) + ((g.nx * (cy + g.ny * cz)) << g.sxs);
+        }
+        int nc = 0;
+#pragma unroll
+        for (int rr = 0; rr < 9; ++rr) nc += sl.O[rr * LF + (j + 2) * sx] - sl.O[rr * LF + (j - 1) * sx];
+        cand += (unsigned long long)(nc - 1);
+        if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+          const float sc = -me.w * p.kp.f_ts;  // the walk summed wf (x_s - x_t)
+          write_output<UPD>(p.out, g, gs, me, r.x * p.kp.phi_scale, sc * r.y, sc * r.z, sc * r.w, fold);
+        } else {
+          write_output<UPD>(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f, fold);
+        }
+      };
       for (;;) {
         int b = 0;
-        if (lane == 0) b = atomicAdd(&sl.meta[6], 32);
+        if (lane == 0) b = atomicAdd(&sl.meta[6], 32 * TPL);
         b = __shfl_sync(0xffffffffu, b, 0);
         if (b >= ntargets) break;
-        const int T = b + lane;
+        const int T = b + lane * TPL;  // the lane's first target (TPL consecutive ones)
         if (T < ntargets) {
           const int gs = t0 + T;
           if (jb < ja) {  // fallback round: cell ja from global memory
-            fallback_target<KERNEL, UPD>(gs, x0 - 1 + ja, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand, p.pairs, p.plane);
+#pragma unroll
+            for (int k = 0; k < TPL; ++k)
+              if (T + k < ntargets)
+                fallback_target<KERNEL, UPD>(gs + k, x0 - 1 + ja, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand,
+                                             p.pairs, p.plane);
             if (T == 0) ++fallbacks;
-          } else {
-            // cell of the target: last j in [ja, jb] with O4[j sx] <= gs
-            int lo_ = ja, hi_ = jb;
-            while (lo_ < hi_) {
-              const int mid = (lo_ + hi_ + 1) >> 1;
-              if (O4[mid * sx] <= gs) lo_ = mid; else hi_ = mid - 1;
-            }
-            const int j = lo_;
-            const int tp = sl.rb[4] - (O4[(ja - 1) * sx] >> 1) + (gs >> 1);  // the target's pair
-            const float4 ua = sl.S[tp], ub = sl.SB[tp];
-            const float4 me = (gs & 1) ? make_float4(ua.y, ua.w, ub.y, ub.w) : make_float4(ua.x, ua.z, ub.x, ub.z);
-            // X sub-cells that can hold a source with |x_s - x_t| < r_c: the fine index is
-            // monotone in x, and x_t - r_c / x_t + r_c are rounded outward, so every skipped
-            // source has |dx| >= r_c exactly (reading R18)
-            bool bad = false;
-            const int flo = fine_x_global(g, __fsub_rd(me.x, rc), bad) - f0;
-            const int fhi = fine_x_global(g, __fadd_ru(me.x, rc), bad) - f0;
-            // (the CANDIDATE test kernel counts every candidate: no pruning)
-            const int klo = KERNEL == PI_K_CANDIDATE ? (j - 1) * sx : min(max(flo, (j - 1) * sx), (j + 2) * sx - 1);
-            const int khi = KERNEL == PI_K_CANDIDATE ? (j + 2) * sx - 1 : min(max(fhi, (j - 1) * sx), (j + 2) * sx - 1);
+          } else if (TPL == 1) {
+            int j, klo, khi;
+            float4 me;
+            setup(gs, j, me, klo, khi);
             const float4 r = p.mask ? walk9<KERNEL, true>(sl, LF, sx, ja, klo, khi, me, thr, mc2, p.kp)
                                     : walk9<KERNEL, false>(sl, LF, sx, ja, klo, khi, me, thr, mc2, p.kp);
-            // the target's fine cell (sub-cell of its slot in the home pencil): moves of the
-            // update are counted against it without recomputing it from the position
-            int fold = -1;
-            if (UPD && p.out.pcounts) {
-              int sub = 0;
-              while (sub + 1 < sx && O4[j * sx + sub + 1] <= gs) ++sub;
-              fold = ((x0 - 1 + j) * sx + sub) + ((g.nx * (cy + g.ny * cz)) << g.sxs);
-            }
-            int nc = 0;  // the 27-cell candidates (the unit of the metric, R4), pruned or not
-#pragma unroll
-            for (int rr = 0; rr < 9; ++rr) nc += sl.O[rr * LF + (j + 2) * sx] - sl.O[rr * LF + (j - 1) * sx];
-            cand += (unsigned long long)(nc - 1);
-            if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
-              const float sc = -me.w * p.kp.f_ts;  // the walk summed wf (x_s - x_t)
-              write_output<UPD>(p.out, g, gs, me, r.x * p.kp.phi_scale, sc * r.y, sc * r.z, sc * r.w, fold);
-            } else {
-              write_output<UPD>(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f, fold);
-            }
+            finish(gs, j, me, r);
+          } else {
+            // two consecutive sorted targets: their fine cells are equal or adjacent (the sorted
+            // order is the fine-cell order), so the union of their windows is 5-6 sub-cells
+            const bool two = T + 1 < ntargets;
+            int j0, klo0, khi0, j1, klo1, khi1;
+            float4 me0, me1;
+            setup(gs, j0, me0, klo0, khi0);
+            setup(two ? gs + 1 : gs, j1, me1, klo1, khi1);
+            float4 r0, r1;
+            walk9x2<KERNEL>(sl, LF, sx, ja, min(klo0, klo1), max(khi0, khi1), me0, me1, thr, mc2, p.kp, r0, r1);
+            finish(gs, j0, me0, r0);
+            if (two) finish(gs + 1, j1, me1, r1);
           }
         }
       }
@@ -452,16 +521,22 @@ cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
     return cudaGetLastError();
   };
   const bool upd = p.out.upd != nullptr;
+  // two targets per lane for the cutoff kernels (walk9x2 relies on exact exclusion outside a
+  // target's own window); the CANDIDATE test kernel and masked grids walk one target per lane
+  const bool two = p.tpl == 2 && !p.mask;
   switch (p.kp.kernel) {
     case PI_K_GAUSSIAN:
-      return upd ? go(k_interact_xpencil<PI_K_GAUSSIAN, NC, true>) : go(k_interact_xpencil<PI_K_GAUSSIAN, NC, false>);
+      if (two) return upd ? go(k_interact_xpencil<PI_K_GAUSSIAN, NC, true, 2>) : go(k_interact_xpencil<PI_K_GAUSSIAN, NC, false, 2>);
+      return upd ? go(k_interact_xpencil<PI_K_GAUSSIAN, NC, true, 1>) : go(k_interact_xpencil<PI_K_GAUSSIAN, NC, false, 1>);
     case PI_K_INDICATOR:
-      return upd ? go(k_interact_xpencil<PI_K_INDICATOR, NC, true>)
-                 : go(k_interact_xpencil<PI_K_INDICATOR, NC, false>);
-    case PI_K_LJ: return upd ? go(k_interact_xpencil<PI_K_LJ, NC, true>) : go(k_interact_xpencil<PI_K_LJ, NC, false>);
+      if (two) return upd ? go(k_interact_xpencil<PI_K_INDICATOR, NC, true, 2>) : go(k_interact_xpencil<PI_K_INDICATOR, NC, false, 2>);
+      return upd ? go(k_interact_xpencil<PI_K_INDICATOR, NC, true, 1>) : go(k_interact_xpencil<PI_K_INDICATOR, NC, false, 1>);
+    case PI_K_LJ:
+      if (two) return upd ? go(k_interact_xpencil<PI_K_LJ, NC, true, 2>) : go(k_interact_xpencil<PI_K_LJ, NC, false, 2>);
+      return upd ? go(k_interact_xpencil<PI_K_LJ, NC, true, 1>) : go(k_interact_xpencil<PI_K_LJ, NC, false, 1>);
     default:
-      return upd ? go(k_interact_xpencil<PI_K_CANDIDATE, NC, true>)
-                 : go(k_interact_xpencil<PI_K_CANDIDATE, NC, false>);
+      return upd ? go(k_interact_xpencil<PI_K_CANDIDATE, NC, true, 1>)
+                 : go(k_interact_xpencil<PI_K_CANDIDATE, NC, false, 1>);
   }
 }
 
@@ -494,6 +569,7 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   }
   p.capp = max(16, cap / 2 + 9);  // + one partial pair per run
   p.nslot = a.slots >= 2 ? min(a.slots, MAX_SLOTS) : 2;
+  p.tpl = a.tpl == 2 ? 2 : 1;  // default 1: two per lane measured slower
   const size_t max_smem = 227 * 1024;
   while (xp_smem_bytes(p.L, p.capp, p.sx, p.nslot) > max_smem && p.capp > 64) p.capp -= 32;
   if (xp_smem_bytes(p.L, p.capp, p.sx, p.nslot) > max_smem) return cudaErrorNotSupported;

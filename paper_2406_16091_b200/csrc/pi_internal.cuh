@@ -239,6 +239,7 @@ struct InteractArgs {
   OutDesc out;
   DevCtl *ctl;
   int tx_len, tx_cap, threads, slots;  // tuning (x-pencil)
+  int tpl;                      // tuning (x-pencil): targets per lane (0 = default)
   int fb[3], fb_cap;            // tuning (full load)
 };
 

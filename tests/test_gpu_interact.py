@@ -145,7 +145,9 @@ def test_xpencil_tuning_shapes(algo):
     for tune in (dict(xpencil_len=1), dict(xpencil_len=7, xpencil_cap=300), dict(xpencil_len=64),
                  dict(xpencil_len=16, xpencil_cap=64), dict(threads=256, xpencil_len=5), dict(threads=32),
                  dict(xpencil_cap=16), dict(xpencil_slots=3), dict(xpencil_slots=4, xpencil_len=16),
-                 dict(xpencil_slots=4, threads=256), dict(xpencil_slots=5)):
+                 dict(xpencil_slots=4, threads=256), dict(xpencil_slots=5),
+                 dict(xpencil_targets=2), dict(xpencil_targets=2, xpencil_len=7, xpencil_cap=300),
+                 dict(xpencil_targets=2, xpencil_cap=64), dict(xpencil_targets=2, threads=288)):
         got, ctx = gpu_interact(c, algo, tuning=tune)
         assert_parity(got, want, label=f"{algo} {tune}")
         if algo == "xpencil" and tune.get("xpencil_cap") in (16, 64):
@@ -191,6 +193,10 @@ def test_x_subcells(xs, kernel):
     for algo in ALGOS:
         got, _ = gpu_interact(c, algo, kernel, ctx=ctx)
         assert_parity(got, want, label=f"x_subcells={xs} {kernel} {algo}")
+    ctx.set_tuning(xpencil_targets=2)  # union windows of two consecutive targets per lane
+    got, _ = gpu_interact(c, "xpencil", kernel, ctx=ctx)
+    assert_parity(got, want, label=f"x_subcells={xs} {kernel} xpencil two targets per lane")
+    ctx.set_tuning()
     counts, offsets = (t.cpu().numpy() for t in ctx.get_offsets())
     wc, wo, _ = celllist.binning(celllist.cells(c.x, c.y, c.z, c.grid), c.grid.ncells)
     assert np.array_equal(counts, wc) and np.array_equal(offsets, wo)
