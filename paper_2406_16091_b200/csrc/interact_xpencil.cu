@@ -345,6 +345,15 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         __syncwarp();
       }
       const int jb = choose_round(p, sl, ja, Lseg);
+      // the round's 27-cell candidates (the unit of the metric, R4): n_j (c27_j - 1) per target
+      // cell j (the fallback round's targets count their own)
+      for (int j = ja + lane; j <= jb; j += 32) {
+        int c27 = 0;
+#pragma unroll
+        for (int r = 0; r < 9; ++r) c27 += sl.O[r * LF + (j + 2) * sx] - sl.O[r * LF + (j - 1) * sx];
+        const int nj = sl.O[4 * LF + (j + 1) * sx] - sl.O[4 * LF + j * sx];
+        cand += (unsigned long long)nj * (unsigned long long)(c27 - 1);
+      }
       // run of pencil r: cells ja-1 .. jb+1 (just cell ja's window for a fallback round)
       const int last = jb < ja ? ja : jb;
       int a = 0, len = 0;  // pairs of pencil run `lane`
@@ -409,36 +418,27 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       // staged home pencil) and its X sub-cell window [klo, khi] (reading R18: the fine index is
       // monotone in x and x_t -/+ r_c are rounded outward, so every skipped source has
       // |dx| >= r_c exactly; the CANDIDATE test kernel counts every candidate: no pruning)
-      auto setup = [&](int gs, int &j, float4 &me, int &klo, int &khi) {
-        int lo_ = ja, hi_ = jb;
-        while (lo_ < hi_) {
-          const int mid = (lo_ + hi_ + 1) >> 1;
-          if (O4[mid * sx] <= gs) lo_ = mid; else hi_ = mid - 1;
-        }
-        j = lo_;
+      auto setup = [&](int gs, int &j, int &sub, float4 &me, int &klo, int &khi) {
         const int tp = sl.rb[4] - (O4[(ja - 1) * sx] >> 1) + (gs >> 1);  // the target's pair
         const float4 ua = sl.S[tp], ub = sl.SB[tp];
         me = (gs & 1) ? make_float4(ua.y, ua.w, ub.y, ub.w) : make_float4(ua.x, ua.z, ub.x, ub.z);
         bool bad = false;
+        // its cell and X sub-cell from its position: the binning's own contract (C3) on the
+        // same fp32 value, so no search in the offsets table
+        const int fg = fine_x_global(g, me.x, bad);
+        j = (fg >> g.sxs) - g.gx_off - (x0 - 1);
+        sub = fg & (sx - 1);
         const int flo = fine_x_global(g, __fsub_rd(me.x, rc), bad) - f0;
         const int fhi = fine_x_global(g, __fadd_ru(me.x, rc), bad) - f0;
         klo = KERNEL == PI_K_CANDIDATE ? (j - 1) * sx : min(max(flo, (j - 1) * sx), (j + 2) * sx - 1);
         khi = KERNEL == PI_K_CANDIDATE ? (j + 2) * sx - 1 : min(max(fhi, (j - 1) * sx), (j + 2) * sx - 1);
       };
-      // epilogue: the 27-cell candidate count (the unit of the metric, R4, pruned or not), the
-      // target's fine cell (moves of the update are counted against it without recomputing it
-      // from the position), the output
-      auto finish = [&](int gs, int j, const float4 &me, const float4 &r) {
+      // epilogue: the target's fine cell (moves of the update are counted against it without
+      // recomputing it from the position), the output.  (The 27-cell candidates, the unit of
+      // the metric, are counted per cell by the producer.)
+      auto finish = [&](int gs, int j, int sub, const float4 &me, const float4 &r) {
         int fold = -1;
-        if (UPD && p.out.pcounts) {
-          int sub = 0;
-          while (sub + 1 < sx && O4[j * sx + sub + 1] <= gs) ++sub;
-          fold = ((x0 - 1 + j) * sx + sub) + ((g.nx * (cy + g.ny * cz)) << g.sxs);
-        }
-        int nc = 0;
-#pragma unroll
-        for (int rr = 0; rr < 9; ++rr) nc += sl.O[rr * LF + (j + 2) * sx] - sl.O[rr * LF + (j - 1) * sx];
-        cand += (unsigned long long)(nc - 1);
+        if (UPD && p.out.pcounts) fold = ((x0 - 1 + j) * sx + sub) + ((g.nx * (cy + g.ny * cz)) << g.sxs);
         if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
           const float sc = -me.w * p.kp.f_ts;  // the walk summed wf (x_s - x_t)
           write_output<UPD>(p.out, g, gs, me, r.x * p.kp.phi_scale, sc * r.y, sc * r.z, sc * r.w, fold);
@@ -462,24 +462,24 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
                                              p.pairs, p.plane);
             if (T == 0) ++fallbacks;
           } else if (TPL == 1) {
-            int j, klo, khi;
+            int j, sub, klo, khi;
             float4 me;
-            setup(gs, j, me, klo, khi);
+            setup(gs, j, sub, me, klo, khi);
             const float4 r = p.mask ? walk9<KERNEL, true>(sl, LF, sx, ja, klo, khi, me, thr, mc2, p.kp)
                                     : walk9<KERNEL, false>(sl, LF, sx, ja, klo, khi, me, thr, mc2, p.kp);
-            finish(gs, j, me, r);
+            finish(gs, j, sub, me, r);
           } else {
             // two consecutive sorted targets: their fine cells are equal or adjacent (the sorted
             // order is the fine-cell order), so the union of their windows is 5-6 sub-cells
             const bool two = T + 1 < ntargets;
-            int j0, klo0, khi0, j1, klo1, khi1;
+            int j0, s0, klo0, khi0, j1, s1, klo1, khi1;
             float4 me0, me1;
-            setup(gs, j0, me0, klo0, khi0);
-            setup(two ? gs + 1 : gs, j1, me1, klo1, khi1);
+            setup(gs, j0, s0, me0, klo0, khi0);
+            setup(two ? gs + 1 : gs, j1, s1, me1, klo1, khi1);
             float4 r0, r1;
             walk9x2<KERNEL>(sl, LF, sx, ja, min(klo0, klo1), max(khi0, khi1), me0, me1, thr, mc2, p.kp, r0, r1);
-            finish(gs, j0, me0, r0);
-            if (two) finish(gs + 1, j1, me1, r1);
+            finish(gs, j0, s0, me0, r0);
+            if (two) finish(gs + 1, j1, s1, me1, r1);
           }
         }
       }
