@@ -18,7 +18,7 @@ constexpr size_t ALIGN = 256;
 size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-  size_t ctl, counts, offsets, foffsets, pcounts, tiles, bcur, rec, sid, perm, urec, uid, tidx, outs, io, pairs;
+  size_t ctl, counts, offsets, foffsets, pcounts, ptsum, tiles, bcur, rec, sid, perm, urec, uid, tidx, outs, io, pairs;
   size_t xrec, xid, xperm, msg[4];  // nranks > 1
   size_t total;
 };
@@ -72,6 +72,7 @@ Layout make_layout(const pi_config *cfg) {
   L.offsets = take(sizeof(int32_t) * (size_t)(ncells + 4));
   L.foffsets = take(sizeof(int32_t) * (size_t)(nf + 4));
   L.pcounts = take(sizeof(int32_t) * (size_t)(nf + 4));
+  L.ptsum = take(sizeof(int32_t) * (size_t)(scan_tiles(nf) + 4));
   L.tiles = take(sizeof(unsigned long long) * (size_t)scan_tiles(nf));
   L.bcur = take(sizeof(int32_t) * PART_NB);
   L.rec = take(sizeof(float4) * (size_t)cap);
@@ -154,7 +155,7 @@ struct pi_ctx_s {
   Layout lay;
   unsigned char *ws;
   DevCtl *ctl;
-  int32_t *counts, *offsets, *foffsets, *pcounts, *sid, *perm, *uid, *tidx, *bcur;
+  int32_t *counts, *offsets, *foffsets, *pcounts, *ptsum, *sid, *perm, *uid, *tidx, *bcur;
   unsigned long long *tiles;
   float4 *rec, *urec, *outs, *pairs;
   float *io;
@@ -269,6 +270,7 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   c->offsets = reinterpret_cast<int32_t *>(c->ws + lay.offsets);
   c->foffsets = reinterpret_cast<int32_t *>(c->ws + lay.foffsets);
   c->pcounts = reinterpret_cast<int32_t *>(c->ws + lay.pcounts);
+  c->ptsum = reinterpret_cast<int32_t *>(c->ws + lay.ptsum);
   c->tiles = reinterpret_cast<unsigned long long *>(c->ws + lay.tiles);
   c->rec = reinterpret_cast<float4 *>(c->ws + lay.rec);
   c->sid = reinterpret_cast<int32_t *>(c->ws + lay.sid);
@@ -396,6 +398,7 @@ static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, c
   // the SoA path's scan records the persistent counts; the delta path re-bins from them
   a.pcounts = one && (delta || !rec_in) ? c->pcounts : nullptr;
   c->pcounts_ok = one && (delta || !rec_in);
+  a.ptsum = c->ptsum;
   a.n = n;
   a.n_dev = n_dev;
   a.x = x; a.y = y; a.z = z; a.q = q;
@@ -488,7 +491,10 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.out.sid = c->sid;
   a.out.uid = c->uid;
   a.out.dt = dt;
-  if (integrate && c->pcounts_ok) a.out.pcounts = c->pcounts;  // movers update the persistent counts
+  if (integrate && c->pcounts_ok) {  // movers update the persistent counts and their tile sums
+    a.out.pcounts = c->pcounts;
+    a.out.ptsum = c->ptsum;
+  }
   a.tx_len = c->tune.xpencil_len;
   a.tx_cap = c->tune.xpencil_cap;
   a.threads = c->tune.threads;

@@ -32,6 +32,7 @@ constexpr int COUNT_THREADS = 256;
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 16;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;  // 4096 cells per tile
+static_assert(SCAN_TILE == (1 << SCAN_TILE_SHIFT), "scan tile");
 
 // a1 + a2 over SoA input (pi_bin, arbitrary order): 4 particles per thread through float4
 // loads, one plain atomic per particle (lanes of random-order input rarely share a cell).
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
                                                        int32_t *__restrict__ offsets,
                                                        unsigned long long *__restrict__ status, int num_tiles,
                                                        DevCtl *ctl, int sxs, int32_t *__restrict__ cell_offsets,
-                                                       int32_t *__restrict__ copy) {
+                                                       int32_t *__restrict__ copy, int32_t *__restrict__ tsum) {
   const int sx = 1 << sxs;
   __shared__ int s_tile;
   __shared__ int s_warp[SCAN_THREADS / 32];
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
     }
     if (lane < SCAN_THREADS / 32) s_warp[lane] = wi - ws;  // exclusive warp offsets
     int tile_total = __shfl_sync(0xffffffffu, wi, SCAN_THREADS / 32 - 1);
+    if (tsum && lane == 0) tsum[tile] = tile_total;  // the tile sums of the copy (delta re-binning)
     // publish the aggregate, then look back
     int prefix = 0;
     if (tile == 0) {
@@ -280,6 +282,113 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
       __threadfence();
       unsigned e = s_epoch;
       int m = atomicAdd(&ctl->mc_slot[e & 1], 0);
+      ctl->max_per_cell = m;
+      ctl->mc_slot[(e + 1) & 1] = 0;
+      ctl->scan_tile_ctr = 0;
+      ctl->scan_done_ctr = 0;
+      __threadfence();
+      atomicAdd(&ctl->scan_epoch, 1u);
+    }
+  }
+}
+
+// a3 for the pi_step re-binning: the persistent counts come with their per-tile sums (kept
+// current by the update, like the counts), so a tile's prefix is the sum of the tile sums
+// before it -- at most a few thousand L2-resident ints per block -- and no tile waits on
+// another (the look-back of k_scan was measured as ~30 % of its stall samples, 37 us at 2^24).
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_delta(long long ncells, const int32_t *__restrict__ counts,
+                                                             const int32_t *__restrict__ tsum,
+                                                             int32_t *__restrict__ offsets, int num_tiles,
+                                                             DevCtl *ctl, int sxs, int32_t *__restrict__ cell_offsets,
+                                                             int32_t *__restrict__ copy) {
+  const int sx = 1 << sxs;
+  __shared__ int s_warp[SCAN_THREADS / 32];
+  __shared__ int s_pre[SCAN_THREADS / 32];
+  __shared__ unsigned s_epoch;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;
+  if (tid == 0) s_epoch = *((volatile unsigned *)&ctl->scan_epoch);
+  const long long base = (long long)tile * SCAN_TILE + (long long)tid * SCAN_ITEMS;
+  int v[SCAN_ITEMS];
+  if (base + SCAN_ITEMS <= ncells) {
+    const int4 *p = reinterpret_cast<const int4 *>(counts + base);
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS / 4; ++k) {
+      const int4 a = p[k];
+      v[4 * k] = a.x; v[4 * k + 1] = a.y; v[4 * k + 2] = a.z; v[4 * k + 3] = a.w;
+      reinterpret_cast<int4 *>(copy + base)[k] = a;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+      const long long c = base + k;
+      v[k] = c < ncells ? counts[c] : 0;
+      if (c < ncells) copy[c] = v[k];
+    }
+  }
+  int pre = 0;  // sum of the tile sums before this tile
+  for (int k = tid; k < tile; k += SCAN_THREADS) pre += __ldcg(tsum + k);
+  int mx = 0, sum = 0, grp = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    sum += v[k];
+    grp += v[k];
+    if (((k + 1) & (sx - 1)) == 0) {
+      mx = max(mx, grp);
+      grp = 0;
+    }
+  }
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  if (lane == 0) s_pre[warp] = pre;
+  __syncthreads();
+  if (lane == 0) atomicMax(&ctl->mc_slot[s_epoch & 1], mx);
+  int woff = 0, prefix = 0;
+#pragma unroll
+  for (int w = 0; w < SCAN_THREADS / 32; ++w) {
+    woff += w < warp ? s_warp[w] : 0;
+    prefix += s_pre[w];
+  }
+  int run = prefix + woff + incl - sum;
+  int outv[SCAN_ITEMS];
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) { outv[k] = run; run += v[k]; }
+  if (base + SCAN_ITEMS <= ncells) {
+    int4 *p = reinterpret_cast<int4 *>(offsets + base);
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS / 4; ++k)
+      p[k] = make_int4(outv[4 * k], outv[4 * k + 1], outv[4 * k + 2], outv[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k)
+      if (base + k < ncells) offsets[base + k] = outv[k];
+  }
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; k += 1)
+    if ((k & (sx - 1)) == 0 && base + k < ncells) cell_offsets[(base + k) >> sxs] = outv[k];
+  if (base <= ncells - 1 && ncells - 1 < base + SCAN_ITEMS) {  // offsets[Nc] = N
+    offsets[ncells] = run;
+    cell_offsets[ncells >> sxs] = run;
+  }
+  // last block: publish M_C, reset the counters, advance the epoch (as k_scan)
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int done = atomicAdd(&ctl->scan_done_ctr, 1);
+    if (done == num_tiles - 1) {
+      __threadfence();
+      const unsigned e = s_epoch;
+      const int m = atomicAdd(&ctl->mc_slot[e & 1], 0);
       ctl->max_per_cell = m;
       ctl->mc_slot[(e + 1) & 1] = 0;
       ctl->scan_tile_ctr = 0;
@@ -455,8 +564,8 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
   const int sgrid = grid_for(a.n, COUNT_THREADS);
   float *pairs = reinterpret_cast<float *>(a.pairs_out);
   if (a.delta) {  // pi_step re-binning from the persistent counts: no count pass
-    k_scan<true><<<tiles, SCAN_THREADS, 0, s>>>(nf, a.pcounts, a.foffsets, a.tile_status, tiles, a.ctl, g.sxs,
-                                                a.offsets, a.counts);
+    k_scan_delta<<<tiles, SCAN_THREADS, 0, s>>>(nf, a.pcounts, a.ptsum, a.foffsets, tiles, a.ctl, g.sxs, a.offsets,
+                                                a.counts);
     if (a.n > 0)
       k_scatter<false><<<sgrid, COUNT_THREADS, 0, s>>>(a.n, a.rec_in, a.id_in, g, a.counts, a.foffsets, a.rec_out,
                                                        a.sid_out, a.perm_out, a.perm_in, a.n_dev, pairs,
@@ -467,7 +576,7 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
     if (a.n > 0)
       k_count_aos<<<sgrid, COUNT_THREADS, 0, s>>>(a.n, a.rec_in, g, a.counts, a.ctl, a.n_dev);
     k_scan<true><<<tiles, SCAN_THREADS, 0, s>>>(nf, a.counts, a.foffsets, a.tile_status, tiles, a.ctl, g.sxs,
-                                                a.offsets, a.pcounts);
+                                                a.offsets, a.pcounts, a.pcounts ? a.ptsum : nullptr);
     if (a.n > 0)
       k_scatter<false><<<sgrid, COUNT_THREADS, 0, s>>>(a.n, a.rec_in, a.id_in, g, a.counts, a.foffsets, a.rec_out,
                                                        a.sid_out, a.perm_out, a.perm_in, a.n_dev, pairs,
@@ -484,7 +593,7 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
     k_count_soa<<<grid_for((a.n + 3) / 4, COUNT_THREADS), COUNT_THREADS, 0, s>>>(a.n, a.x, a.y, a.z, g, a.counts,
                                                                                  a.ctl);
   k_scan<true><<<tiles, SCAN_THREADS, 0, s>>>(nf, a.counts, a.foffsets, a.tile_status, tiles, a.ctl, g.sxs,
-                                              a.offsets, a.pcounts);
+                                              a.offsets, a.pcounts, a.pcounts ? a.ptsum : nullptr);
   if (a.n == 0) return cudaGetLastError();
   const long long want = std::min<long long>(PART_NB, std::max<long long>(1, a.n >> 17));
   int bsh = 0;

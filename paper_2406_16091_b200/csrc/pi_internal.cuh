@@ -134,6 +134,9 @@ __device__ __forceinline__ float integrate1(float x, float f, float dt, float lo
 // ------------------------------------------------------------------------------------
 // Output descriptor of the interaction kernels.
 // ------------------------------------------------------------------------------------
+// a3 scans fine counts in tiles of 2^SCAN_TILE_SHIFT (binning.cu)
+constexpr int SCAN_TILE_SHIFT = 12;
+
 struct OutDesc {
   float4 *sorted;          // [n] (phi, fx, fy, fz) in sorted order (always written)
   const int32_t *perm;     // sorted slot -> caller index (NULL: no caller-order outputs)
@@ -146,6 +149,7 @@ struct OutDesc {
   // persistent per-sub-cell counts of the sorted state (nullable): a particle whose fine cell
   // changes in the update moves one count from its old to its new fine cell
   int32_t *pcounts;
+  int32_t *ptsum;          // their per-scan-tile sums (kept current with them)
 };
 
 // UPD = false compiles the pi_step update out (kernels specialised for pi_interact).
@@ -178,6 +182,10 @@ __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, in
       if (f1 != f0) {
         atomicSub(o.pcounts + f0, 1);
         atomicAdd(o.pcounts + f1, 1);
+        if ((f0 >> SCAN_TILE_SHIFT) != (f1 >> SCAN_TILE_SHIFT)) {
+          atomicSub(o.ptsum + (f0 >> SCAN_TILE_SHIFT), 1);
+          atomicAdd(o.ptsum + (f1 >> SCAN_TILE_SHIFT), 1);
+        }
       }
     }
   }
@@ -217,6 +225,8 @@ struct BinArgs {
                                 // (layout of InteractArgs::pairs)
   long long pair_plane;         // float4 elements per plane of the pair array
   int32_t *pcounts;             // [ncells sx] persistent counts of the sorted state (one rank)
+  int32_t *ptsum;               // [scan tiles] their per-tile sums (written by the count paths'
+                                // scan, kept current by the pi_step update)
   bool delta;                   // AoS re-binning from pcounts (kept current by the pi_step update)
   DevCtl *ctl;
 };

@@ -23,7 +23,7 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for name in a.configs.split(","):
     c = synth.make_config(name)
     g = c.grid
-    ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=c.n, device="cuda")
+    ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=c.n, device="cuda", x_subcells=int(os.environ.get("XSUB", "0")))
     t = [torch.from_numpy(v).cuda() for v in (c.x, c.y, c.z, c.q)]
     byts = 48.0 * c.n + 12.0 * g.ncells
     ms = []
