@@ -212,6 +212,20 @@ PI_API pi_status pi_step(pi_ctx ctx, pi_algo algo, float dt);
 PI_API pi_status pi_run_host(pi_ctx ctx, pi_algo algo, int64_t n, const float *x, const float *y, const float *z,
                       const float *q, float *phi, float *fx, float *fy, float *fz);
 
+/* Pipelined end-to-end runs on HOST buffers, for a stream of independent inputs (one rank):
+ * pi_run_host_submit enqueues what pi_run_host does -- H2D x,y,z,q, bin, interact, D2H
+ * phi,F -- and returns without synchronising; up to two runs are in flight (a third submit
+ * first waits for the oldest), each on its own half of the workspace's I/O buffers, with the
+ * host->device copies on one internal stream, the kernels on the context stream and the
+ * device->host copies on another, so run k+1's upload and run k-1's download overlap run k's
+ * kernels (PCIe is full duplex).  The caller keeps every host buffer of a run valid and
+ * unread until pi_run_host_wait, which blocks until all submitted runs' outputs are in host
+ * memory (and orders the context stream after them).  Same arguments and errors as
+ * pi_run_host; the introspection calls see the state of the latest submitted run.         */
+PI_API pi_status pi_run_host_submit(pi_ctx ctx, pi_algo algo, int64_t n, const float *x, const float *y,
+                                    const float *z, const float *q, float *phi, float *fx, float *fy, float *fz);
+PI_API pi_status pi_run_host_wait(pi_ctx ctx);
+
 /* Introspection (device pointers, async, any may be NULL):
  *   cell_of[n]  cell index of each particle of the last pi_bin, caller order   (a1)
  *   counts[Nc]  particles per cell (local grid when nranks > 1)                (a2)

@@ -52,6 +52,8 @@ SIGNATURES = {
     "pi_interact": (ctypes.c_int, [P, ctypes.c_int, P, P, P, P]),
     "pi_step": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_float]),
     "pi_run_host": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int64, P, P, P, P, P, P, P, P]),
+    "pi_run_host_submit": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int64, P, P, P, P, P, P, P, P]),
+    "pi_run_host_wait": (ctypes.c_int, [P]),
     "pi_get_binning": (ctypes.c_int, [P, P, P, P, P]),
     "pi_get_particles": (ctypes.c_int, [P, P, P, P, P, P, P, P, P, P]),
     "pi_get_stats": (ctypes.c_int, [P, ctypes.POINTER(pi_stats)]),

@@ -82,7 +82,7 @@ Layout make_layout(const pi_config *cfg) {
   L.uid = take(sizeof(int32_t) * (size_t)cap);
   L.tidx = take(sizeof(int32_t) * (size_t)cap);
   L.outs = take(sizeof(float4) * (size_t)cap);
-  L.io = take(sizeof(float) * 8 * (size_t)cap);
+  L.io = take(sizeof(float) * 16 * (size_t)cap);  // two sets of x,y,z,q in + phi,F out (host paths)
   L.pairs = take(sizeof(float4) * 2 * (size_t)pair_plane_of(cap));  // two planes (A: x, y; B: z, q)
   if (cfg->nranks > 1) {
     L.xrec = take(sizeof(float4) * (size_t)cap);
@@ -170,6 +170,10 @@ struct pi_ctx_s {
   SlabState slab;    // nranks > 1
   cudaEvent_t ev[4][2];  // phase timing: 0 bin, 1 interact, 2 exchange, 3 host copies
   bool ev_used[4];
+  // pipelined host runs (pi_run_host_submit/_wait): copy streams and per-set events
+  cudaStream_t h2d, d2h;
+  cudaEvent_t ev_sub, ev_in[2], ev_binned[2], ev_out[2], ev_done[2];
+  long long rh_issued, rh_done;
   char err[512];
 };
 
@@ -370,6 +374,17 @@ pi_status pi_destroy(pi_ctx c) {
     for (int k = 0; k < 4; ++k)
       for (int b = 0; b < 2; ++b)
         if (c->ev[k][b]) cudaEventDestroy(c->ev[k][b]);
+    if (c->h2d) {
+      cudaEventDestroy(c->ev_sub);
+      for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(c->ev_in[b]);
+        cudaEventDestroy(c->ev_binned[b]);
+        cudaEventDestroy(c->ev_out[b]);
+        cudaEventDestroy(c->ev_done[b]);
+      }
+      cudaStreamDestroy(c->h2d);
+      cudaStreamDestroy(c->d2h);
+    }
     delete c->slab.tr;
   }
   delete c;
@@ -595,6 +610,86 @@ pi_status pi_run_host(pi_ctx c, pi_algo algo, int64_t n, const float *x, const f
       return cuda_check(c, e, "pi_run_host D2H");
   phase_end(c, 3);
   return cuda_check(c, cudaStreamSynchronize(c->stream), "pi_run_host sync");
+}
+
+// Pipelined host runs: run k uses I/O set k % 2 of the workspace.  H2D on its own stream,
+// bin + interact on the context stream, D2H on a third stream, ordered by events, so the
+// copies of run k+1 (host -> device) and run k-1 (device -> host) overlap run k's kernels.
+static pi_status rh_wait_one(pi_ctx c) {
+  if (c->rh_done >= c->rh_issued) return PI_OK;
+  const int k = (int)(c->rh_done % 2);
+  cudaError_t e = cudaEventSynchronize(c->ev_done[k]);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, c->ev_done[k], 0);
+  ++c->rh_done;
+  return cuda_check(c, e, "pi_run_host_wait");
+}
+
+pi_status pi_run_host_submit(pi_ctx c, pi_algo algo, int64_t n, const float *x, const float *y, const float *z,
+                             const float *q, float *phi, float *fx, float *fy, float *fz) {
+  if (!c) return PI_EINVAL;
+  if (c->cfg.nranks > 1) return fail(c, PI_EINVAL, "pi_run_host_submit: one rank only (use pi_run_host)");
+  if (n < 0 || n > c->cfg.capacity) return fail(c, PI_ECAPACITY, "n out of range");
+  if (n > 0 && (!x || !y || !z || !q)) return fail(c, PI_EINVAL, "NULL host input");
+  cudaError_t e = cudaSuccess;
+  if (!c->h2d) {  // first use: the copy streams and events
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_sub, cudaEventDisableTiming);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+      e = cudaEventCreateWithFlags(&c->ev_in[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_binned[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_out[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done[b], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_check(c, e, "pi_run_host_submit: streams/events");
+  }
+  if (c->rh_issued - c->rh_done >= 2) {  // both I/O sets in flight: wait for the older run
+    pi_status s = rh_wait_one(c);
+    if (s != PI_OK) return s;
+  }
+  const long long run = c->rh_issued;
+  const int k = (int)(run % 2);
+  const size_t cap = (size_t)c->cfg.capacity;
+  float *in = c->io + (size_t)k * 8 * cap, *out = in + 4 * cap;
+  const size_t bytes = sizeof(float) * (size_t)n;
+  const float *src[4] = {x, y, z, q};
+  float *hout[4] = {phi, fx, fy, fz};
+  // host -> device after the work already on the context stream, and after run-2's binning
+  // has consumed this input set
+  e = cudaEventRecord(c->ev_sub, c->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->h2d, c->ev_sub, 0);
+  if (e == cudaSuccess && run >= 2) e = cudaStreamWaitEvent(c->h2d, c->ev_binned[k], 0);
+  for (int a = 0; a < 4 && e == cudaSuccess && n > 0; ++a)
+    e = cudaMemcpyAsync(in + a * cap, src[a], bytes, cudaMemcpyHostToDevice, c->h2d);
+  if (e == cudaSuccess) e = cudaEventRecord(c->ev_in[k], c->h2d);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, c->ev_in[k], 0);
+  if (e != cudaSuccess) return cuda_check(c, e, "pi_run_host_submit H2D");
+  pi_status s = pi_bin(c, n, in, in + cap, in + 2 * cap, in + 3 * cap, nullptr);
+  if (s != PI_OK) return s;
+  e = cudaEventRecord(c->ev_binned[k], c->stream);
+  // the output set is free once run-2's results reached the host
+  if (e == cudaSuccess && run >= 2) e = cudaStreamWaitEvent(c->stream, c->ev_done[k], 0);
+  if (e != cudaSuccess) return cuda_check(c, e, "pi_run_host_submit");
+  s = pi_interact(c, algo, phi ? out : nullptr, fx ? out + cap : nullptr, fy ? out + 2 * cap : nullptr,
+                  fz ? out + 3 * cap : nullptr);
+  if (s != PI_OK) return s;
+  e = cudaEventRecord(c->ev_out[k], c->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->d2h, c->ev_out[k], 0);
+  for (int a = 0; a < 4 && e == cudaSuccess && n > 0; ++a)
+    if (hout[a]) e = cudaMemcpyAsync(hout[a], out + a * cap, bytes, cudaMemcpyDeviceToHost, c->d2h);
+  if (e == cudaSuccess) e = cudaEventRecord(c->ev_done[k], c->d2h);
+  if (e != cudaSuccess) return cuda_check(c, e, "pi_run_host_submit D2H");
+  ++c->rh_issued;
+  return PI_OK;
+}
+
+pi_status pi_run_host_wait(pi_ctx c) {
+  if (!c) return PI_EINVAL;
+  while (c->rh_done < c->rh_issued) {
+    pi_status s = rh_wait_one(c);
+    if (s != PI_OK) return s;
+  }
+  return PI_OK;
 }
 
 pi_status pi_get_binning(pi_ctx c, int32_t *cell_of, int32_t *counts, int32_t *offsets, int32_t *perm) {

@@ -230,3 +230,26 @@ def test_lj_softening_coincident_and_params(algo):
     c2.grid = synth.Grid(dims=c2.grid.dims, w=c2.grid.w, lj_r=0.8 * c2.grid.w, lj_eps=0.03 * c2.grid.w, lj_e0=0.7)
     got, _ = gpu_interact(c2, algo, "lj")
     assert_parity(got, oracle_interact(c2, "lj"), label=f"lj params {algo}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_run_host_paths(algo):
+    """End-to-end calls on pinned host buffers: the synchronous pi_run_host and the pipelined
+    pi_run_host_submit/_wait (two runs in flight on alternating I/O sets, a third submit waits
+    for the oldest) give the oracle's values for each of several different inputs."""
+    clouds = [synth.scaled_uniform(8, (12, 10, 9), seed=s) for s in (21, 22, 23, 24, 25)]
+    wants = [oracle_interact(c) for c in clouds]
+    cap = max(c.n for c in clouds)
+    ctx = ctx_for(clouds[0], capacity=cap)
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    hin = [[pin(a) for a in (c.x, c.y, c.z, c.q)] for c in clouds]
+    hout = [[torch.full((c.n,), float("nan")).pin_memory() for _ in range(4)] for c in clouds]
+    ctx.run_host(algo, *hin[0], *hout[0])
+    assert_parity(torch.stack(hout[0], 1).numpy(), wants[0], label=f"run_host {algo}")
+    for o in hout[0]:
+        o.fill_(float("nan"))
+    for k in range(len(clouds)):
+        ctx.run_host_submit(algo, *hin[k], *hout[k])
+    ctx.run_host_wait()
+    for k in range(len(clouds)):
+        assert_parity(torch.stack(hout[k], 1).numpy(), wants[k], label=f"run_host_submit {algo} run {k}")
