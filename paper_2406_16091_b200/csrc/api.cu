@@ -18,7 +18,7 @@ constexpr size_t ALIGN = 256;
 size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-  size_t ctl, counts, offsets, foffsets, pcounts, ptsum, tiles, bcur, rec, sid, perm, urec, uid, tidx, outs, io, pairs;
+  size_t ctl, counts, offsets, foffsets, pcounts, ptsum, dense, tiles, bcur, rec, sid, perm, urec, uid, tidx, outs, io, pairs;
   size_t xrec, xid, xperm, msg[4];  // nranks > 1
   size_t total;
 };
@@ -73,6 +73,7 @@ Layout make_layout(const pi_config *cfg) {
   L.foffsets = take(sizeof(int32_t) * (size_t)(nf + 4));
   L.pcounts = take(sizeof(int32_t) * (size_t)(nf + 4));
   L.ptsum = take(sizeof(int32_t) * (size_t)(scan_tiles(nf) + 4));
+  L.dense = take(sizeof(int32_t) * (size_t)(ncells + 4));
   L.tiles = take(sizeof(unsigned long long) * (size_t)scan_tiles(nf));
   L.bcur = take(sizeof(int32_t) * PART_NB);
   L.rec = take(sizeof(float4) * (size_t)cap);
@@ -155,7 +156,7 @@ struct pi_ctx_s {
   Layout lay;
   unsigned char *ws;
   DevCtl *ctl;
-  int32_t *counts, *offsets, *foffsets, *pcounts, *ptsum, *sid, *perm, *uid, *tidx, *bcur;
+  int32_t *counts, *offsets, *foffsets, *pcounts, *ptsum, *dense, *sid, *perm, *uid, *tidx, *bcur;
   unsigned long long *tiles;
   float4 *rec, *urec, *outs, *pairs;
   float *io;
@@ -275,6 +276,7 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   c->foffsets = reinterpret_cast<int32_t *>(c->ws + lay.foffsets);
   c->pcounts = reinterpret_cast<int32_t *>(c->ws + lay.pcounts);
   c->ptsum = reinterpret_cast<int32_t *>(c->ws + lay.ptsum);
+  c->dense = reinterpret_cast<int32_t *>(c->ws + lay.dense);
   c->tiles = reinterpret_cast<unsigned long long *>(c->ws + lay.tiles);
   c->rec = reinterpret_cast<float4 *>(c->ws + lay.rec);
   c->sid = reinterpret_cast<int32_t *>(c->ws + lay.sid);
@@ -327,6 +329,8 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   }
   // zero the control block, counts (the scan keeps them zero afterwards) and scan status
   cudaError_t e = cudaMemsetAsync(c->ws, 0, lay.rec, c->stream);
+  // the X-pencil's dense-cell list: entries are -1 when free (cellsm.cuh)
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + lay.dense, 0xff, lay.tiles - lay.dense, c->stream);
   if (e != cudaSuccess) {
     pi_status s = cuda_check(c, e, "pi_create memset");
     delete c;
@@ -515,6 +519,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.threads = c->tune.threads;
   a.slots = c->tune.xpencil_slots;
   a.tpl = c->tune.xpencil_targets;
+  a.dense = c->dense;
   a.fb[0] = c->tune.fullload_box[0]; a.fb[1] = c->tune.fullload_box[1]; a.fb[2] = c->tune.fullload_box[2];
   a.fb_cap = c->tune.fullload_cap;
   cudaError_t e = cudaMemsetAsync(&c->ctl->fallback_cells, 0,

@@ -21,6 +21,7 @@
 //   * capacity: the slot is sized from the mean density (+15 %) instead of M_C (:353), so there
 //     is no device->host read-back; a row whose 9 pencils do not fit is split into rounds
 //     along X, and a cell whose window alone does not fit takes the global-memory path.
+#include "cellsm.cuh"
 #include "interact_common.cuh"
 
 #ifdef XP_PROFILE  // development counters (tools/build_prof.sh, tools/xp_prof.py)
@@ -61,6 +62,7 @@ struct XpParams {
   int capp;          // staged source pairs per slot
   int nslot;         // staging slots (2..MAX_SLOTS)
   int tpl;           // targets per consumer lane (1 or 2)
+  int32_t *dense;    // cells whose window alone does not fit a slot: listed for Par-Cell-SM
   int nseg;          // segments per X row
   long long nitems;  // rows x segments
 };
@@ -332,6 +334,8 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
           if (lane == 0) {
             sl.meta[0] = 1;
             mbar_arrive(&full[s]);
+            __threadfence();  // this block's listed cells precede its "producer done"
+            atomicAdd(&p.ctl->pad[2], 1ull);
           }
           break;
         }
@@ -344,7 +348,20 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         for (int k = lane; k < 9 * LF; k += 32) sl.O[k] = prev.O[k];
         __syncwarp();
       }
-      const int jb = choose_round(p, sl, ja, Lseg);
+      int jb = choose_round(p, sl, ja, Lseg);
+      // a cell whose window alone does not fit the slot is listed for the Par-Cell-SM pass
+      // (interact_cellsm.cu) and skipped; an item that ends in such cells leaves an empty round
+      while (jb < ja && ja <= Lseg) {
+        if (lane == 0) {
+          const unsigned long long k = atomicAdd(&p.ctl->pad[0], 1ull);
+          p.dense[k] = (x0 - 1 + ja) + g.nx * (cy + g.ny * cz);
+          ++fallbacks;
+        }
+        ++ja;
+        if (ja <= Lseg) jb = choose_round(p, sl, ja, Lseg);
+      }
+      const bool none = ja > Lseg;  // empty round (no targets)
+      if (none) jb = ja - 1;
       // the round's 27-cell candidates (the unit of the metric, R4): n_j (c27_j - 1) per target
       // cell j (the fallback round's targets count their own)
       for (int j = ja + lane; j <= jb; j += 32) {
@@ -357,9 +374,9 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       // run of pencil r: cells ja-1 .. jb+1 (just cell ja's window for a fallback round)
       const int last = jb < ja ? ja : jb;
       int a = 0, len = 0;  // pairs of pencil run `lane`
-      if (lane < 9) {
+      if (lane < 9 && !none) {
         a = sl.O[lane * LF + (ja - 1) * sx] >> 1;
-        len = jb < ja ? 0 : ((sl.O[lane * LF + (last + 2) * sx] + 1) >> 1) - a;
+        len = ((sl.O[lane * LF + (last + 2) * sx] + 1) >> 1) - a;
       }
       int incl = len;
 #pragma unroll
@@ -374,7 +391,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         sl.meta[0] = 0;
         sl.meta[1] = ja;
         sl.meta[2] = jb;
-        sl.meta[3] = sl.O[4 * LF + (last + 1) * sx] - sl.O[4 * LF + ja * sx];
+        sl.meta[3] = none ? 0 : sl.O[4 * LF + (last + 1) * sx] - sl.O[4 * LF + ja * sx];
         sl.meta[4] = x0;
         sl.meta[5] = cy | (cz << 16);
         sl.meta[6] = 0;
@@ -491,6 +508,23 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     }
   }
 
+  // the dense cells listed by the producers of all blocks (Par-Cell-SM, cellsm.cuh), in the
+  // staging memory this block no longer uses
+  __syncthreads();
+  {
+    CsParams cp;
+    cp.rec = p.rec;
+    cp.pairs = p.pairs;
+    cp.plane = p.plane;
+    cp.offsets = p.offsets;
+    cp.list = p.dense;
+    cp.g = p.g;
+    cp.kp = p.kp;
+    cp.out = p.out;
+    cp.ctl = p.ctl;
+    cellsm_phase<KERNEL, UPD, (NC + 1) * 32>(cp, slots);
+  }
+
   // statistics: warp-level sums, spread over CAND_SLOTS counters
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -505,7 +539,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
 
 template <int NC>
 cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
-  const size_t smem = xp_smem_bytes(p.L, p.capp, p.sx, p.nslot);
+  const size_t smem = max(xp_smem_bytes(p.L, p.capp, p.sx, p.nslot), CS_SMEM + 128);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(kern);
     if (e != cudaSuccess) return e;
@@ -569,6 +603,7 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   }
   p.capp = max(16, cap / 2 + 9);  // + one partial pair per run
   p.nslot = a.slots >= 2 ? min(a.slots, MAX_SLOTS) : 2;
+  p.dense = a.dense;
   p.tpl = a.tpl == 2 ? 2 : 1;  // default 1: two per lane measured slower
   const size_t max_smem = 227 * 1024;
   while (xp_smem_bytes(p.L, p.capp, p.sx, p.nslot) > max_smem && p.capp > 64) p.capp -= 32;

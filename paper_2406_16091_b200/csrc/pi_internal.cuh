@@ -53,7 +53,8 @@ struct DevCtl {
   // everything from here on is reset before each interaction
   unsigned long long fallback_cells;
   unsigned long long xp_items;        // X-pencil work-item counter (reset before each launch)
-  unsigned long long pad[2];
+  unsigned long long pad[4];         // X-pencil dense cells: listed [0], Par-Cell-SM ticket [1],
+                                      // blocks whose producer finished [2]
   unsigned long long cand_slots[64];  // candidates (C) of the last interaction, spread counters
 };
 constexpr int CAND_SLOTS = 64;
@@ -250,6 +251,7 @@ struct InteractArgs {
   DevCtl *ctl;
   int tx_len, tx_cap, threads, slots;  // tuning (x-pencil)
   int tpl;                      // tuning (x-pencil): targets per lane (0 = default)
+  int32_t *dense;               // [ncells] cells listed by the X-pencil for the Par-Cell-SM pass
   int fb[3], fb_cap;            // tuning (full load)
 };
 

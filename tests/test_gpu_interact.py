@@ -253,3 +253,26 @@ def test_run_host_paths(algo):
     ctx.run_host_wait()
     for k in range(len(clouds)):
         assert_parity(torch.stack(hout[k], 1).numpy(), wants[k], label=f"run_host_submit {algo} run {k}")
+
+
+# (Lennard-Jones is left out here: on this clustered cloud one particle's force is dominated by
+# a single pair near the LJ force zero, 12 s^5 = 6 s^2, where the fp32 term itself cancels to
+# ~1e-4 relative -- all three strategies agree on it to 1e-7, the fp64 oracle does not, and the
+# per-particle bound 1e-4 sum|c_ij| (R14) has no room for cancellation inside one term.  The LJ
+# path of the Par-Cell-SM pass is checked on uniform input in test_gpu_step.)
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate"])
+@pytest.mark.parametrize("xcap", [16, 200])
+def test_dense_cells_par_cell_sm(kernel, xcap):
+    """Cells whose window alone does not fit an X-pencil slot are listed and computed by the
+    Par-Cell-SM pass: a staging capacity of 16 lists every cell, 200 some.
+    Clustered cloud (configs[3] recipe, small): parity, exact integer counts, exact candidates."""
+    qk = "ones" if kernel in ("indicator", "candidate") else "pos"
+    c = synth.clustered(1 << 14, synth.Grid(dims=(16, 16, 16), w=1 / 16), seed=240616094, qkind=qk)
+    want = oracle_interact(c, kernel)
+    got, ctx = gpu_interact(c, "xpencil", kernel, tuning=dict(xpencil_cap=xcap))
+    assert_parity(got, want, label=f"dense {kernel} cap {xcap}")
+    if qk == "ones":  # integer outputs: exact
+        assert np.array_equal(got[:, 0], want["P" if kernel == "indicator" else "C"].astype(np.float64))
+    st = ctx.stats()
+    assert st["fallback_cells"] > 0
+    assert st["candidates"] == int(want["C"].sum())

@@ -19,16 +19,21 @@ def state(ctx):
     return {k: v.cpu().numpy() for k, v in p.items()}
 
 
-@pytest.mark.parametrize("algo,kernel,xs", [("global", "gaussian", 0), ("xpencil", "gaussian", 0),
-                                             ("fullload", "gaussian", 0), ("xpencil", "gaussian", 1),
-                                             ("xpencil", "gaussian", 8), ("xpencil", "lj", 0),
-                                             ("global", "lj", 4)])
-def test_step_matches_oracle(algo, kernel, xs):
+@pytest.mark.parametrize("algo,kernel,xs,tune", [("global", "gaussian", 0, None), ("xpencil", "gaussian", 0, None),
+                                                  ("fullload", "gaussian", 0, None), ("xpencil", "gaussian", 1, None),
+                                                  ("xpencil", "gaussian", 8, None), ("xpencil", "lj", 0, None),
+                                                  ("global", "lj", 4, None),
+                                                  # every cell through the Par-Cell-SM pass
+                                                  ("xpencil", "gaussian", 0, dict(xpencil_cap=16)),
+                                                  ("xpencil", "lj", 2, dict(xpencil_cap=16))])
+def test_step_matches_oracle(algo, kernel, xs, tune):
     """Three steps, each checked against the oracle at the GPU's pre-step state; the re-binning
     (counts carried by the update, R18 sub-cells) must be bit-exact per cell afterwards."""
     c = synth.make_config("c0")
     g = c.grid
     ctx = ctx_for(c, kernel, x_subcells=xs)
+    if tune:
+        ctx.set_tuning(**tune)
     ctx.bin(*to_dev(c))
     s0 = state(ctx)                                   # sorted state before the step
     # dt: a few % of the particles change sub-cell each step (the Gaussian forces of c0 are
