@@ -67,15 +67,16 @@ struct XpParams {
   long long nitems;  // rows x segments
 };
 
-// Slot: SA[capp] | SB[capp] float4 (source pairs, planes A and B) | meta[16] | O[9][LF] | rb[16],
+// Slot: SA[capp] | SB[capp] float4 (source pairs, planes A and B) | meta[16] | O[9][LF] | rb[32],
 // LF = (L+2) sx + 1
 //   O[r][k]  global offsets of pencil r (= (dy + 1) + 3 (dz + 1)) at the fine (X sub-cell)
 //            boundary k of the cells x0-1 .. x0+L; the cell boundary j is O[r][j sx]
-//   rb[r]    first staged pair of pencil r's run in S (rb[9] = total)
+//   rb[r]    first staged pair of pencil r's run in S (rb[9] = total); rb[16 + r] = rb[r] minus
+//            the global pair index of the run's first record: staged pair of global pair k
 // meta: 0 stop (1), 1 ja, 2 jb (target cells ja..jb of the item in this round; jb < ja: the
 //       global-memory fallback for cell ja), 3 ntargets, 4 x0, 5 cy | cz << 16, 6 batch counter
 __host__ __device__ inline int lf_of(int L, int sx) { return (L + 2) * sx + 1; }
-__host__ __device__ inline int slot_words(int L, int sx) { return (META + 9 * lf_of(L, sx) + 16 + 3) & ~3; }
+__host__ __device__ inline int slot_words(int L, int sx) { return (META + 9 * lf_of(L, sx) + 32 + 3) & ~3; }
 __host__ __device__ inline size_t slot_bytes(int L, int capp, int sx) {
   return (size_t)capp * 32 + (size_t)slot_words(L, sx) * 4;
 }
@@ -206,7 +207,7 @@ __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, 
   for (int r = 0; r < 9; ++r) {
     const int a = sl.O[r * LF + klo], b = sl.O[r * LF + khi + 1];
     if (b <= a) continue;
-    const int base = sl.rb[r] - (sl.O[r * LF + (ja - 1) * sx] >> 1);
+    const int base = sl.rb[16 + r];
     const int p0 = base + (a >> 1), pl = base + ((b - 1) >> 1);  // first and last pair
     if (!MASK) {
       int q = p0;
@@ -266,7 +267,7 @@ __device__ __forceinline__ void walk9x2(const Slot &sl, int LF, int sx, int ja, 
   for (int r = 0; r < 9; ++r) {
     const int a = sl.O[r * LF + klo], b = sl.O[r * LF + khi + 1];
     if (b <= a) continue;
-    const int base = sl.rb[r] - (sl.O[r * LF + (ja - 1) * sx] >> 1);
+    const int base = sl.rb[16 + r];
     const int p0 = base + (a >> 1), pl = base + ((b - 1) >> 1);  // first and last pair
     int q = p0;
     for (; q + 1 <= pl; q += 2) {
@@ -385,7 +386,10 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         if (lane >= o) incl += t;
       }
       const int total = __shfl_sync(0xffffffffu, incl, 8);
-      if (lane < 9) sl.rb[lane] = incl - len;
+      if (lane < 9) {
+        sl.rb[lane] = incl - len;
+        sl.rb[16 + lane] = incl - len - a;
+      }
       if (lane == 0) {
         sl.rb[9] = total;
         sl.meta[0] = 0;
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       // monotone in x and x_t -/+ r_c are rounded outward, so every skipped source has
       // |dx| >= r_c exactly; the CANDIDATE test kernel counts every candidate: no pruning)
       auto setup = [&](int gs, int &j, int &sub, float4 &me, int &klo, int &khi) {
-        const int tp = sl.rb[4] - (O4[(ja - 1) * sx] >> 1) + (gs >> 1);  // the target's pair
+        const int tp = sl.rb[16 + 4] + (gs >> 1);  // the target's staged pair
         const float4 ua = sl.S[tp], ub = sl.SB[tp];
         me = (gs & 1) ? make_float4(ua.y, ua.w, ub.y, ub.w) : make_float4(ua.x, ua.z, ub.x, ub.z);
         bool bad = false;
