@@ -659,10 +659,14 @@ pi_status pi_run_host_submit(pi_ctx c, pi_algo algo, int64_t n, const float *x, 
   const size_t bytes = sizeof(float) * (size_t)n;
   const float *src[4] = {x, y, z, q};
   float *hout[4] = {phi, fx, fy, fz};
-  // host -> device after the work already on the context stream, and after run-2's binning
-  // has consumed this input set
-  e = cudaEventRecord(c->ev_sub, c->stream);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->h2d, c->ev_sub, 0);
+  // host -> device once run-2's binning has consumed this input set; with no run in flight,
+  // also after the work already on the context stream (the caller's timing events, say).
+  // (Waiting on the context stream while a run is in flight would order this upload after
+  // that run's kernels and serialise the pipeline.)
+  if (c->rh_issued == c->rh_done) {
+    e = cudaEventRecord(c->ev_sub, c->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->h2d, c->ev_sub, 0);
+  }
   if (e == cudaSuccess && run >= 2) e = cudaStreamWaitEvent(c->h2d, c->ev_binned[k], 0);
   for (int a = 0; a < 4 && e == cudaSuccess && n > 0; ++a)
     e = cudaMemcpyAsync(in + a * cap, src[a], bytes, cudaMemcpyHostToDevice, c->h2d);
