@@ -276,3 +276,27 @@ def test_dense_cells_par_cell_sm(kernel, xcap):
     st = ctx.stats()
     assert st["fallback_cells"] > 0
     assert st["candidates"] == int(want["C"].sum())
+
+
+@pytest.mark.parametrize("name", ["c3", "c2_ppc1", "c2_ppc64"])
+def test_full_size_sampled(name):
+    """BASELINE configs at full size (2^24 particles) in the bench's launch configuration,
+    sampled targets against the oracle: configs[3] clustered (M_C ~ 370: the X-pencil lists its
+    densest cells for the Par-Cell-SM pass) and the two ends of the configs[2] ppc sweep (1 and
+    64 per cell).  Candidates are checked against the oracle's count on the sample's cells'
+    closed form at full size: sum over cells of n_c (sum of the 27 neighbours' counts) - N."""
+    c = synth.make_config(name)
+    ctx = ctx_for(c)
+    got, ctx = gpu_interact(c, "xpencil", ctx=ctx)
+    sample = np.random.default_rng(5).choice(c.n, 4000, replace=False)
+    want = oracle_interact(c, targets=sample)
+    assert_parity(got[sample], want, label=f"{name} xpencil")
+    counts, _ = (t.cpu().numpy().astype(np.int64) for t in ctx.get_offsets())
+    nx, ny, nz = c.grid.dims
+    n3 = counts.reshape(nz, ny, nx)
+    pad = np.pad(n3, 1)
+    nb = sum(pad[1 + dz:1 + dz + nz, 1 + dy:1 + dy + ny, 1 + dx:1 + dx + nx]
+             for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1))
+    assert ctx.stats()["candidates"] == int((n3 * nb).sum() - c.n)
+    if name == "c3":
+        assert ctx.stats()["fallback_cells"] > 0
