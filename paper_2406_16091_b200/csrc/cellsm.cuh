@@ -31,6 +31,7 @@ struct CsParams {
   const float4 *pairs;  // pair planes A | B
   long long plane;
   const int32_t *offsets;
+  bool from_rec;           // stage from the records (full load: the pair array may be stale)
   int32_t *list;           // listed cells (local linear ids), -1 when free
   Geom g;
   KParams kp;
@@ -84,8 +85,17 @@ __device__ void cs_targets(const CsParams &p, int t0, int tbase, int nt, int P, 
       int r = 0;
       while (r < 8 && rstart[r + 1] <= ci) ++r;
       const long long gp = (long long)rpa[r] + (ci - rstart[r]);
-      cp_async16(A + i, p.pairs + gp);
-      cp_async16(B + i, p.pairs + p.plane + gp);
+      if (p.from_rec) {  // the pair from two records; halves outside the run are inert
+        const float4 inert = make_float4(1.0e30f, 1.0e30f, 1.0e30f, 0.f);
+        const long long k0 = 2 * gp, k1 = k0 + 1;
+        const float4 u = (k0 >= ra[r] && k0 < rb[r]) ? __ldg(p.rec + k0) : inert;
+        const float4 v = (k1 >= ra[r] && k1 < rb[r]) ? __ldg(p.rec + k1) : inert;
+        A[i] = make_float4(u.x, v.x, u.y, v.y);
+        B[i] = make_float4(u.z, v.z, u.w, v.w);
+      } else {
+        cp_async16(A + i, p.pairs + gp);
+        cp_async16(B + i, p.pairs + p.plane + gp);
+      }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -124,7 +134,7 @@ __device__ void cs_targets(const CsParams &p, int t0, int tbase, int nt, int P, 
 // block's producer has finished (ctl->pad[2] == gridDim.x).  An entry is published by its value
 // (entries are -1 when free: a reader spins on its entry, then frees it for the next launch).
 template <int KERNEL, bool UPD, int NT>
-__device__ void cellsm_phase(const CsParams &p, unsigned char *smem) {
+__device__ void cellsm_phase(const CsParams &p, unsigned char *smem, bool wait_producers) {
   float4 *A = reinterpret_cast<float4 *>(smem), *B = A + CS_CHUNK;
   int *rstart = reinterpret_cast<int *>(A + 2 * CS_CHUNK);  // [10]
   int *rpa = rstart + 10, *ra = rpa + 9, *rb = ra + 9;      // [9] each
@@ -145,7 +155,7 @@ __device__ void cellsm_phase(const CsParams &p, unsigned char *smem) {
           list[t] = -1;
           break;
         }
-        if (*done >= gridDim.x) {
+        if (!wait_producers || *done >= gridDim.x) {
           __threadfence();
           if ((unsigned long long)t < *cnt) continue;
           break;  // every producer finished and the list is exhausted
@@ -196,6 +206,14 @@ __device__ void cellsm_phase(const CsParams &p, unsigned char *smem) {
         cs_targets<KERNEL, UPD, 1, NT>(p, t0, tbase, nt, P, rstart, rpa, ra, rb, A, B);
     }
   }
+}
+
+// The same pass as a kernel of its own, after a non-persistent kernel has listed its cells
+// (full load: a block whose sub-box does not fit lists the box's non-empty cells).
+template <int KERNEL, bool UPD>
+__global__ void __launch_bounds__(256) k_cellsm_list(CsParams p) {
+  extern __shared__ __align__(16) unsigned char cs_raw[];
+  cellsm_phase<KERNEL, UPD, 256>(p, cs_raw, false);
 }
 
 }  // namespace pi

@@ -18,6 +18,7 @@
 //   * compute: one thread per PAIR of targets of one cell (packed f32x2 registers), the 27
 //     candidate cells walked as 9 contiguous 3-cell runs of shared memory, every source a
 //     broadcast scalar operand (12 packed-fp32 ops + 2 MUFU.EX2 per source and 2 candidates).
+#include "cellsm.cuh"
 #include "interact_common.cuh"
 
 namespace pi {
@@ -33,6 +34,7 @@ struct FlParams {
   DevCtl *ctl;
   int bx, by, bz;  // interior sub-box dims (cells)
   int cap;         // staged records
+  int32_t *dense;  // cells of the boxes that do not fit: listed for the Par-Cell-SM pass
 };
 
 // smem: mbarrier (16 B) | ints: Lst[R+1] | O[R][Bx+3] | Ppre[C+1] | ctl[8] | S[cap] (16-B aligned)
@@ -190,14 +192,17 @@ __global__ void __launch_bounds__(NT) k_interact_fullload(FlParams p) {
   const int total = Lst[R];
   const int npairs = Ppre[C];
   if (total > p.cap) {
-    // the staged sub-box does not fit: every target of the block through global memory
-    for (int c = 0; c < C; ++c) {
+    // the staged sub-box does not fit (dense input): its non-empty cells are listed for the
+    // Par-Cell-SM pass that follows this kernel (cellsm.cuh, k_cellsm_list)
+    for (int c = tid; c < C; c += NT) {
       const int cx = c % bx, cy = (c / bx) % by, cz = c / (bx * by);
       if (cx >= ex || cy >= ey || cz >= ez) continue;
       const long long home = (long long)g.nx * (y0 + cy + (long long)g.ny * (z0 + cz));
       const int t_lo = __ldg(p.offsets + home + x0 + cx), t_hi = __ldg(p.offsets + home + x0 + cx + 1);
-      for (int t = t_lo + tid; t < t_hi; t += NT)
-        fallback_target<KERNEL>(t, x0 + cx, y0 + cy, z0 + cz, p.rec, p.offsets, g, p.kp, p.out, cand);
+      if (t_hi > t_lo) {
+        const unsigned long long k = atomicAdd(&p.ctl->pad[0], 1ull);
+        p.dense[k] = (int)(home + x0 + cx);
+      }
     }
     if (tid == 0) atomicAdd(&p.ctl->fallback_cells, (unsigned long long)(ex * ey * ez));
   } else {
@@ -308,6 +313,7 @@ cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const Inte
   p.kp = k;
   p.out = a.out;
   p.ctl = a.ctl;
+  p.dense = a.dense;
   const double ppc = (double)a.n_est / (double)g.ncells;
   const size_t max_smem = 227 * 1024;
   if (a.fb[0] > 0 || a.fb[1] > 0 || a.fb[2] > 0) {
@@ -345,9 +351,37 @@ cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const Inte
   if (fl_smem_bytes(p.bx, p.by, p.bz, 64) > max_smem) return cudaErrorNotSupported;
   while (fl_smem_bytes(p.bx, p.by, p.bz, p.cap) > max_smem && p.cap > 64) p.cap -= 32;
   const int threads = a.threads == 128 ? 128 : (a.threads == 512 ? 512 : 256);
-  if (threads == 128) return launch_nt<128>(p, s);
-  if (threads == 512) return launch_nt<512>(p, s);
-  return launch_nt<256>(p, s);
+  cudaError_t e = threads == 128 ? launch_nt<128>(p, s) : (threads == 512 ? launch_nt<512>(p, s) : launch_nt<256>(p, s));
+  if (e != cudaSuccess) return e;
+  // the cells of the boxes that did not fit (usually none: one atomic per block)
+  CsParams cp;
+  cp.rec = a.rec;
+  cp.pairs = a.pairs;
+  cp.plane = a.pair_plane;
+  cp.offsets = a.offsets;
+  cp.from_rec = true;
+  cp.list = a.dense;
+  cp.g = g;
+  cp.kp = k;
+  cp.out = a.out;
+  cp.ctl = a.ctl;
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e2 = allow_max_smem(kern);
+    if (e2 != cudaSuccess) return e2;
+    int dev = 0, sms = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, CS_SMEM);
+    kern<<<sms * (occ > 0 ? occ : 1), 256, CS_SMEM, s>>>(cp);
+    return cudaGetLastError();
+  };
+  const bool upd = a.out.upd != nullptr;
+  switch (k.kernel) {
+    case PI_K_GAUSSIAN: return upd ? go(k_cellsm_list<PI_K_GAUSSIAN, true>) : go(k_cellsm_list<PI_K_GAUSSIAN, false>);
+    case PI_K_INDICATOR: return upd ? go(k_cellsm_list<PI_K_INDICATOR, true>) : go(k_cellsm_list<PI_K_INDICATOR, false>);
+    case PI_K_LJ: return upd ? go(k_cellsm_list<PI_K_LJ, true>) : go(k_cellsm_list<PI_K_LJ, false>);
+    default: return upd ? go(k_cellsm_list<PI_K_CANDIDATE, true>) : go(k_cellsm_list<PI_K_CANDIDATE, false>);
+  }
 }
 
 }  // namespace pi

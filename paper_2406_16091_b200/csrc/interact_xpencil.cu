@@ -526,7 +526,8 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     cp.kp = p.kp;
     cp.out = p.out;
     cp.ctl = p.ctl;
-    cellsm_phase<KERNEL, UPD, (NC + 1) * 32>(cp, slots);
+    cp.from_rec = false;
+    cellsm_phase<KERNEL, UPD, (NC + 1) * 32>(cp, slots, true);
   }
 
   // statistics: warp-level sums, spread over CAND_SLOTS counters
