@@ -199,8 +199,6 @@ __device__ __forceinline__ void scalar_term(const KParams &kp, float r2, float q
   }
 }
 
-// Fallback for a target whose cell window does not fit the staging buffer: Par-Part-NoLoop
-// over global memory (Alg. 1) for target slot t in cell (cx, cy, cz).
 // Record s of the sorted state: from the records, or (rec == NULL) from the f32x2 pair array
 // A[k] = (x_2k, x_2k+1, y_2k, y_2k+1) = pairs[k], B[k] = (z.., z.., q.., q..) = pairs[plane + k].
 __device__ __forceinline__ float4 sorted_rec(const float4 *__restrict__ rec, const float4 *__restrict__ pairs,
@@ -208,56 +206,6 @@ __device__ __forceinline__ float4 sorted_rec(const float4 *__restrict__ rec, con
   if (rec) return __ldg(rec + s);
   const float4 a = __ldg(pairs + (s >> 1)), b = __ldg(pairs + plane + (s >> 1));
   return (s & 1) ? make_float4(a.y, a.w, b.y, b.w) : make_float4(a.x, a.z, b.x, b.z);
-}
-
-template <int KERNEL, bool UPD = true>
-__device__ void fallback_target(int t, int cx, int cy, int cz, const float4 *__restrict__ rec,
-                                const int32_t *__restrict__ offsets, const Geom &g, const KParams &kp,
-                                const OutDesc &out, unsigned long long &cand,
-                                const float4 *__restrict__ pairs = nullptr, long long plane = 0) {
-  const int xlo = max(cx - 1, 0), xhi = min(cx + 1, g.nx - 1);
-  const float4 me = sorted_rec(rec, pairs, plane, t);
-  float phi = 0.f, fx = 0.f, fy = 0.f, fz = 0.f;
-  for (int dz = -1; dz <= 1; ++dz) {
-    const int z = cz + dz;
-    if (z < 0 || z >= g.nz) continue;
-    for (int dy = -1; dy <= 1; ++dy) {
-      const int y = cy + dy;
-      if (y < 0 || y >= g.ny) continue;
-      const long long row = (long long)g.nx * (y + (long long)g.ny * z);
-      const int lo_ = __ldg(offsets + row + xlo), hi_ = __ldg(offsets + row + xhi + 1);
-      cand += (unsigned long long)(hi_ - lo_);
-      for (int s = lo_; s < hi_; ++s) {
-        if (s == t) continue;
-        const float4 o = sorted_rec(rec, pairs, plane, s);
-        const float dx = me.x - o.x, dy2 = me.y - o.y, dz2 = me.z - o.z;
-        const float r2 = fmaf(dz2, dz2, fmaf(dy2, dy2, dx * dx));
-        if (KERNEL == PI_K_CANDIDATE) {
-          phi += o.w;
-        } else if (r2 < kp.rc2) {
-          if (KERNEL == PI_K_INDICATOR) {
-            phi += o.w;
-          } else {
-            float w, wf;
-            scalar_term<KERNEL>(kp, r2, o.w, w, wf);
-            phi += w;
-            fx = fmaf(wf, dx, fx);
-            fy = fmaf(wf, dy2, fy);
-            fz = fmaf(wf, dz2, fz);
-          }
-        }
-      }
-    }
-  }
-  cand -= 1;
-  if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
-    const float sc = me.w * kp.f_ts;
-    phi *= kp.phi_scale;
-    fx *= sc; fy *= sc; fz *= sc;
-  } else {
-    fx = fy = fz = 0.f;
-  }
-  write_output<UPD>(out, g, t, me, phi, fx, fy, fz);
 }
 
 }  // namespace pi

@@ -73,8 +73,8 @@ struct XpParams {
 //            boundary k of the cells x0-1 .. x0+L; the cell boundary j is O[r][j sx]
 //   rb[r]    first staged pair of pencil r's run in S (rb[9] = total); rb[16 + r] = rb[r] minus
 //            the global pair index of the run's first record: staged pair of global pair k
-// meta: 0 stop (1), 1 ja, 2 jb (target cells ja..jb of the item in this round; jb < ja: the
-//       global-memory fallback for cell ja), 3 ntargets, 4 x0, 5 cy | cz << 16, 6 batch counter
+// meta: 0 stop (1), 1 ja, 2 jb (target cells ja..jb of the item in this round; an empty round
+//       has ntargets = 0), 3 ntargets, 4 x0, 5 cy | cz << 16, 6 batch counter
 __host__ __device__ inline int lf_of(int L, int sx) { return (L + 2) * sx + 1; }
 __host__ __device__ inline int slot_words(int L, int sx) { return (META + 9 * lf_of(L, sx) + 32 + 3) & ~3; }
 __host__ __device__ inline size_t slot_bytes(int L, int capp, int sx) {
@@ -474,15 +474,8 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         if (b >= ntargets) break;
         const int T = b + lane * TPL;  // the lane's first target (TPL consecutive ones)
         if (T < ntargets) {
-          const int gs = t0 + T;
-          if (jb < ja) {  // fallback round: cell ja from global memory
-#pragma unroll
-            for (int k = 0; k < TPL; ++k)
-              if (T + k < ntargets)
-                fallback_target<KERNEL, UPD>(gs + k, x0 - 1 + ja, cy, cz, p.rec, p.offsets, g, p.kp, p.out, cand,
-                                             p.pairs, p.plane);
-            if (T == 0) ++fallbacks;
-          } else if (TPL == 1) {
+          const int gs = t0 + T;  // (rounds always have jb >= ja: cells that do not fit are listed)
+          if (TPL == 1) {
             int j, sub, klo, khi;
             float4 me;
             setup(gs, j, sub, me, klo, khi);
