@@ -39,13 +39,14 @@ struct CsParams {
   DevCtl *ctl;
 };
 
+// staged pairs q0, q0 + G, q0 + 2G, ... of the chunk (G source groups, see cs_targets)
 template <int KERNEL, int TPT>
 __device__ __forceinline__ void cs_compute(const float4 *__restrict__ A, const float4 *__restrict__ B, int n,
-                                           const float4 *me, const float thr, const float mc2, const KParams &kp,
-                                           p2 (*acc)[4]) {
-  int q = 0;
-  for (; q + 1 < n; q += 2) {
-    const SrcPair s0 = load_pair(A, B, q), s1 = load_pair(A, B, q + 1);
+                                           int q0, int G, const float4 *me, const float thr, const float mc2,
+                                           const KParams &kp, p2 (*acc)[4]) {
+  int q = q0;
+  for (; q + G < n; q += 2 * G) {
+    const SrcPair s0 = load_pair(A, B, q), s1 = load_pair(A, B, q + G);
 #pragma unroll
     for (int k = 0; k < TPT; ++k) {
       src_eval<KERNEL>(s0, me[k].x, me[k].y, me[k].z, thr, mc2, acc[k][0], acc[k][1], acc[k][2], acc[k][3], &kp);
@@ -60,18 +61,23 @@ __device__ __forceinline__ void cs_compute(const float4 *__restrict__ A, const f
   }
 }
 
+// Targets tbase .. of the cell: TPT per thread, or (TPT = 1, a cell of at most NT / 2 targets)
+// G source groups of NT / G threads, group g taking every G-th staged pair, so a small cell
+// keeps every thread busy; the groups' partial sums meet in shared memory at the end.
 template <int KERNEL, bool UPD, int TPT, int NT>
 __device__ void cs_targets(const CsParams &p, int t0, int tbase, int nt, int P, const int *rstart, const int *rpa,
                            const int *ra, const int *rb, float4 *A, float4 *B) {
   const int tid = threadIdx.x;
   const float thr = p.kp.rc2, mc2 = -p.kp.c2;
+  const int G = TPT == 1 ? max(1, min(4, NT / max(nt - tbase, 1))) : 1, tpg = NT / G;
+  const int gi = tid / tpg, ti = tid - gi * tpg;  // source group, target slot in the group
   float4 me[TPT];
   bool ok[TPT];
   p2 acc[TPT][4];
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
-    const int t = tbase + tid + k * NT;
-    ok[k] = t < nt;
+    const int t = tbase + ti + k * NT;
+    ok[k] = gi < G && t < nt;
     me[k] = ok[k] ? sorted_rec(p.rec, p.pairs, p.plane, t0 + t) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[k][c] = pk(0.f);
@@ -110,15 +116,32 @@ __device__ void cs_targets(const CsParams &p, int t0, int tbase, int nt, int P, 
       }
     }
     __syncthreads();
-    if (any) cs_compute<KERNEL, TPT>(A, B, n, me, thr, mc2, p.kp, acc);
+    if (any) cs_compute<KERNEL, TPT>(A, B, n, gi, G, me, thr, mc2, p.kp, acc);
+  }
+  if (G > 1) {  // the groups' partial sums, summed by group 0 (reusing the staging buffer)
+    __syncthreads();
+    float4 *red = A;
+    if (ok[0] && gi > 0)
+      red[(gi - 1) * tpg + ti] = make_float4(lo(acc[0][0]) + hi(acc[0][0]), lo(acc[0][1]) + hi(acc[0][1]),
+                                             lo(acc[0][2]) + hi(acc[0][2]), lo(acc[0][3]) + hi(acc[0][3]));
+    __syncthreads();
+    if (ok[0] && gi == 0) {
+      for (int h = 1; h < G; ++h) {
+        const float4 v = red[(h - 1) * tpg + ti];
+        acc[0][0] = add2(acc[0][0], pk(v.x, 0.f));
+        acc[0][1] = add2(acc[0][1], pk(v.y, 0.f));
+        acc[0][2] = add2(acc[0][2], pk(v.z, 0.f));
+        acc[0][3] = add2(acc[0][3], pk(v.w, 0.f));
+      }
+    }
   }
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
-    if (!ok[k]) continue;
+    if (!ok[k] || gi > 0) continue;
     const float phi = lo(acc[k][0]) + hi(acc[k][0]) - self_term<KERNEL>(me[k].w, p.kp);
     const float sx_ = lo(acc[k][1]) + hi(acc[k][1]), sy_ = lo(acc[k][2]) + hi(acc[k][2]);
     const float sz_ = lo(acc[k][3]) + hi(acc[k][3]);
-    const int t = t0 + tbase + tid + k * NT;
+    const int t = t0 + tbase + ti + k * NT;
     if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
       const float sc = -me[k].w * p.kp.f_ts;  // the walk summed wf (x_s - x_t)
       write_output<UPD>(p.out, p.g, t, me[k], phi * p.kp.phi_scale, sc * sx_, sc * sy_, sc * sz_);
