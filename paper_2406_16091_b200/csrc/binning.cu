@@ -295,19 +295,18 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(long long ncells, int32_t
 // a3 for the pi_step re-binning: the persistent counts come with their per-tile sums (kept
 // current by the update, like the counts), so a tile's prefix is the sum of the tile sums
 // before it -- at most a few thousand L2-resident ints per block -- and no tile waits on
-// another (the look-back of k_scan was measured as ~30 % of its stall samples, 37 us at 2^24).
+// another (the look-back of k_scan was measured as ~30 % of its stall samples, 37 us at 2^24);
+// M_C goes straight into ctl->max_per_cell (zeroed before the launch): no last-block step.
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_delta(long long ncells, const int32_t *__restrict__ counts,
                                                              const int32_t *__restrict__ tsum,
-                                                             int32_t *__restrict__ offsets, int num_tiles,
+                                                             int32_t *__restrict__ offsets,
                                                              DevCtl *ctl, int sxs, int32_t *__restrict__ cell_offsets,
                                                              int32_t *__restrict__ copy) {
   const int sx = 1 << sxs;
   __shared__ int s_warp[SCAN_THREADS / 32];
   __shared__ int s_pre[SCAN_THREADS / 32];
-  __shared__ unsigned s_epoch;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tile = blockIdx.x;
-  if (tid == 0) s_epoch = *((volatile unsigned *)&ctl->scan_epoch);
   const long long base = (long long)tile * SCAN_TILE + (long long)tid * SCAN_ITEMS;
   int v[SCAN_ITEMS];
   if (base + SCAN_ITEMS <= ncells) {
@@ -352,7 +351,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_delta(long long ncells, c
   if (lane == 31) s_warp[warp] = incl;
   if (lane == 0) s_pre[warp] = pre;
   __syncthreads();
-  if (lane == 0) atomicMax(&ctl->mc_slot[s_epoch & 1], mx);
+  if (lane == 0) atomicMax(&ctl->max_per_cell, mx);  // zeroed before the launch (launch_bin)
   int woff = 0, prefix = 0;
 #pragma unroll
   for (int w = 0; w < SCAN_THREADS / 32; ++w) {
@@ -379,23 +378,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_delta(long long ncells, c
   if (base <= ncells - 1 && ncells - 1 < base + SCAN_ITEMS) {  // offsets[Nc] = N
     offsets[ncells] = run;
     cell_offsets[ncells >> sxs] = run;
-  }
-  // last block: publish M_C, reset the counters, advance the epoch (as k_scan)
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const int done = atomicAdd(&ctl->scan_done_ctr, 1);
-    if (done == num_tiles - 1) {
-      __threadfence();
-      const unsigned e = s_epoch;
-      const int m = atomicAdd(&ctl->mc_slot[e & 1], 0);
-      ctl->max_per_cell = m;
-      ctl->mc_slot[(e + 1) & 1] = 0;
-      ctl->scan_tile_ctr = 0;
-      ctl->scan_done_ctr = 0;
-      __threadfence();
-      atomicAdd(&ctl->scan_epoch, 1u);
-    }
   }
 }
 
@@ -564,7 +546,9 @@ cudaError_t launch_bin(const Geom &g, const BinArgs &a, cudaStream_t s) {
   const int sgrid = grid_for(a.n, COUNT_THREADS);
   float *pairs = reinterpret_cast<float *>(a.pairs_out);
   if (a.delta) {  // pi_step re-binning from the persistent counts: no count pass
-    k_scan_delta<<<tiles, SCAN_THREADS, 0, s>>>(nf, a.pcounts, a.ptsum, a.foffsets, tiles, a.ctl, g.sxs, a.offsets,
+    cudaError_t e = cudaMemsetAsync(&a.ctl->max_per_cell, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    k_scan_delta<<<tiles, SCAN_THREADS, 0, s>>>(nf, a.pcounts, a.ptsum, a.foffsets, a.ctl, g.sxs, a.offsets,
                                                 a.counts);
     if (a.n > 0)
       k_scatter<false><<<sgrid, COUNT_THREADS, 0, s>>>(a.n, a.rec_in, a.id_in, g, a.counts, a.foffsets, a.rec_out,
