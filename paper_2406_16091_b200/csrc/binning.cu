@@ -493,6 +493,46 @@ __global__ void __launch_bounds__(COUNT_THREADS) k_scatter(long long n, const fl
                                                             float *__restrict__ pairs_out = nullptr,
                                                             long long plane = 0) {
   if (n_dev) n = *n_dev;
+  if (!GATHER) {
+    // two records per thread and iteration (i, i + blockDim.x): the two dependent chains
+    // (record -> cell -> rank atomic -> offset -> stores) overlap
+    const long long step = 2LL * gridDim.x * blockDim.x;
+    for (long long i0 = 2LL * blockIdx.x * blockDim.x; i0 < n; i0 += step) {
+      const long long ia = i0 + threadIdx.x, ib = ia + blockDim.x;
+      const bool oka = ia < n, okb = ib < n;
+      const float4 ra = oka ? __ldg(rec_in + ia) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 rb = okb ? __ldg(rec_in + ib) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int32_t ida = oka ? (id_in ? __ldg(id_in + ia) : (int32_t)ia) : 0;
+      const int32_t idb = okb ? (id_in ? __ldg(id_in + ib) : (int32_t)ib) : 0;
+      bool b = false;
+      const int lina = fine_lin(g, ra.x, ra.y, ra.z, b), linb = fine_lin(g, rb.x, rb.y, rb.z, b);
+      const int rka = run_take(counts, lina, oka);
+      const int rkb = run_take(counts, linb, okb);
+      const int sa = oka ? __ldg(offsets + lina) + rka : 0, sb = okb ? __ldg(offsets + linb) + rkb : 0;
+      auto put = [&](long long i, const float4 &r, int slot, int32_t id) {
+        if (rec_out) rec_out[slot] = r;
+        if (pairs_out) {
+          float *pa = pairs_out + 4 * (long long)(slot >> 1) + (slot & 1);
+          float *pb = pa + 4 * plane;
+          pa[0] = r.x;
+          pa[2] = r.y;
+          pb[0] = r.z;
+          pb[2] = r.w;
+          if (slot == n - 1 && !(slot & 1)) {
+            pa[1] = 1.0e30f;
+            pa[3] = 1.0e30f;
+            pb[1] = 1.0e30f;
+            pb[3] = 0.f;
+          }
+        }
+        sid_out[slot] = id;
+        if (perm_out) perm_out[slot] = perm_in ? __ldg(perm_in + i) : (int32_t)i;
+      };
+      if (oka) put(ia, ra, sa, ida);
+      if (okb) put(ib, rb, sb, idb);
+    }
+    return;
+  }
   for (long long i0 = (long long)blockIdx.x * blockDim.x; i0 < n; i0 += (long long)gridDim.x * blockDim.x) {
     const long long i = i0 + threadIdx.x;
     const bool ok = i < n;
