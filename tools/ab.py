@@ -10,9 +10,10 @@ cfg = sys.argv[2] if len(sys.argv) > 2 else "c1"
 algo = sys.argv[3] if len(sys.argv) > 3 else "xpencil"
 c = synth.make_config(cfg); g = c.grid
 ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=c.n, x_subcells=int(os.environ.get('XSUB', '0')))
-if os.environ.get('TPL') or os.environ.get('LEN') or os.environ.get('TGT') or os.environ.get('THREADS'):
+if any(os.environ.get(k) for k in ("TPL", "LEN", "TGT", "THREADS", "CAP")):
     ctx.set_tuning(xpencil_slots=int(os.environ.get('TPL', '0')), threads=int(os.environ.get('THREADS', '0')),
-                   xpencil_len=int(os.environ.get('LEN', '0')), xpencil_targets=int(os.environ.get('TGT', '0')))
+                   xpencil_len=int(os.environ.get('LEN', '0')), xpencil_targets=int(os.environ.get('TGT', '0')),
+                   xpencil_cap=int(os.environ.get('CAP', '0')))
 t = [torch.from_numpy(v).cuda() for v in (c.x, c.y, c.z, c.q)]
 ctx.bin(*t)
 _, fx, fy, fz = ctx.interact(algo)
@@ -32,4 +33,4 @@ step = run(lambda: ctx.step(algo, dt))
 st = ctx.stats()
 ctx.bin(*t)
 inter = run(lambda: ctx.interact(algo, out=False))
-print(f"{os.path.basename(L.LIBPATH):20s} slots={os.environ.get('TPL', '0')} len={os.environ.get('LEN', '0')} thr={os.environ.get('THREADS', '0')} tgt={os.environ.get('TGT', '0')} sx={os.environ.get('XSUB', '0')} {cfg} {algo}: step {step*1e3:7.1f} us (bin {st['bin_ms']*1e3:6.1f} interact {st['interact_ms']*1e3:6.1f})  pi_interact {inter*1e3:7.1f} us")
+print(f"{os.path.basename(L.LIBPATH):20s} slots={os.environ.get('TPL', '0')} len={os.environ.get('LEN', '0')} thr={os.environ.get('THREADS', '0')} tgt={os.environ.get('TGT', '0')} cap={os.environ.get('CAP', '0')} sx={os.environ.get('XSUB', '0')} {cfg} {algo}: step {step*1e3:7.1f} us (bin {st['bin_ms']*1e3:6.1f} interact {st['interact_ms']*1e3:6.1f})  pi_interact {inter*1e3:7.1f} us")
