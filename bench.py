@@ -400,8 +400,8 @@ def run_ours(a):
     else:
         # pi_step, one rank: scan of the carried counts (k_scan_delta), scatter (which also
         # writes the X-pencil's source pairs), interact (+ integrate fused); plus two memsets of
-        # the control block, not counted.  Other strategies read the records: same 3 kernels.
-        launches = 3
+        # the control block, not counted.  The full load adds its Par-Cell-SM kernel.
+        launches = 3 + (1 if a.algo == "fullload" else 0)
     line = {
         "metric": METRIC,
         "value": value,
