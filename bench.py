@@ -395,8 +395,9 @@ def run_ours(a):
     e2e_value = c_e2e / (e2e_mean * 1e-3)
 
     if world > 1:
-        # reset, migrate, append, reset, ghosts, append, count, scan, scatter (+ pairify), interact
-        launches = 10 + (1 if a.algo == "xpencil" else 0)
+        # reset, migrate, append, reset, ghosts, append, count, scan, scatter (which writes the
+        # source pairs), interact (+ the full load's Par-Cell-SM kernel); NCCL's own kernels not counted
+        launches = 10 + (1 if a.algo == "fullload" else 0)
     else:
         # pi_step, one rank: scan of the carried counts (k_scan_delta), scatter (which also
         # writes the X-pencil's source pairs), interact (+ integrate fused); plus two memsets of
