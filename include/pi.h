@@ -214,8 +214,8 @@ PI_API pi_status pi_run_host(pi_ctx ctx, pi_algo algo, int64_t n, const float *x
 
 /* Pipelined end-to-end runs on HOST buffers, for a stream of independent inputs (one rank):
  * pi_run_host_submit enqueues what pi_run_host does -- H2D x,y,z,q, bin, interact, D2H
- * phi,F -- and returns without synchronising; up to two runs are in flight (a third submit
- * first waits for the oldest), each on its own half of the workspace's I/O buffers, with the
+ * phi,F -- and returns without synchronising; up to three runs are in flight (a fourth submit
+ * first waits for the oldest), each on its own third of the workspace's I/O buffers, with the
  * host->device copies on one internal stream, the kernels on the context stream and the
  * device->host copies on another, so run k+1's upload and run k-1's download overlap run k's
  * kernels (PCIe is full duplex).  The caller keeps every host buffer of a run valid and

@@ -189,7 +189,7 @@ class Context:
 
     def run_host_submit(self, algo, x, y, z, q, phi, fx, fy, fz):
         """Pipelined end-to-end run on host (pinned) float32 tensors: enqueued, not synchronised; keep the
-        tensors alive and unread until run_host_wait() (two runs in flight, pi.h)."""
+        tensors alive and unread until run_host_wait() (three runs in flight, pi.h)."""
         a = L.ALGOS[algo] if isinstance(algo, str) else int(algo)
         n = int(x.numel())
         self._check(self._lib.pi_run_host_submit(self._h, a, n, _ptr(x), _ptr(y), _ptr(z), _ptr(q), _ptr(phi),

@@ -13,6 +13,8 @@ using namespace pi;
 
 namespace {
 
+constexpr int RH_SETS = 3;  // pipelined host runs in flight (pi_run_host_submit)
+
 constexpr size_t ALIGN = 256;
 
 size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
@@ -83,7 +85,7 @@ Layout make_layout(const pi_config *cfg) {
   L.uid = take(sizeof(int32_t) * (size_t)cap);
   L.tidx = take(sizeof(int32_t) * (size_t)cap);
   L.outs = take(sizeof(float4) * (size_t)cap);
-  L.io = take(sizeof(float) * 16 * (size_t)cap);  // two sets of x,y,z,q in + phi,F out (host paths)
+  L.io = take(sizeof(float) * 8 * RH_SETS * (size_t)cap);  // RH_SETS sets of x,y,z,q in + phi,F out (host paths)
   L.pairs = take(sizeof(float4) * 2 * (size_t)pair_plane_of(cap));  // two planes (A: x, y; B: z, q)
   if (cfg->nranks > 1) {
     L.xrec = take(sizeof(float4) * (size_t)cap);
@@ -173,7 +175,7 @@ struct pi_ctx_s {
   bool ev_used[4];
   // pipelined host runs (pi_run_host_submit/_wait): copy streams and per-set events
   cudaStream_t h2d, d2h;
-  cudaEvent_t ev_sub, ev_in[2], ev_binned[2], ev_out[2], ev_done[2];
+  cudaEvent_t ev_sub, ev_in[RH_SETS], ev_binned[RH_SETS], ev_out[RH_SETS], ev_done[RH_SETS];
   long long rh_issued, rh_done;
   char err[512];
 };
@@ -380,7 +382,7 @@ pi_status pi_destroy(pi_ctx c) {
         if (c->ev[k][b]) cudaEventDestroy(c->ev[k][b]);
     if (c->h2d) {
       cudaEventDestroy(c->ev_sub);
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < RH_SETS; ++b) {
         cudaEventDestroy(c->ev_in[b]);
         cudaEventDestroy(c->ev_binned[b]);
         cudaEventDestroy(c->ev_out[b]);
@@ -617,12 +619,12 @@ pi_status pi_run_host(pi_ctx c, pi_algo algo, int64_t n, const float *x, const f
   return cuda_check(c, cudaStreamSynchronize(c->stream), "pi_run_host sync");
 }
 
-// Pipelined host runs: run k uses I/O set k % 2 of the workspace.  H2D on its own stream,
+// Pipelined host runs: run k uses I/O set k % RH_SETS of the workspace.  H2D on its own stream,
 // bin + interact on the context stream, D2H on a third stream, ordered by events, so the
 // copies of run k+1 (host -> device) and run k-1 (device -> host) overlap run k's kernels.
 static pi_status rh_wait_one(pi_ctx c) {
   if (c->rh_done >= c->rh_issued) return PI_OK;
-  const int k = (int)(c->rh_done % 2);
+  const int k = (int)(c->rh_done % RH_SETS);
   cudaError_t e = cudaEventSynchronize(c->ev_done[k]);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, c->ev_done[k], 0);
   ++c->rh_done;
@@ -640,7 +642,7 @@ pi_status pi_run_host_submit(pi_ctx c, pi_algo algo, int64_t n, const float *x, 
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_sub, cudaEventDisableTiming);
-    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    for (int b = 0; b < RH_SETS && e == cudaSuccess; ++b) {
       e = cudaEventCreateWithFlags(&c->ev_in[b], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_binned[b], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_out[b], cudaEventDisableTiming);
@@ -648,12 +650,12 @@ pi_status pi_run_host_submit(pi_ctx c, pi_algo algo, int64_t n, const float *x, 
     }
     if (e != cudaSuccess) return cuda_check(c, e, "pi_run_host_submit: streams/events");
   }
-  if (c->rh_issued - c->rh_done >= 2) {  // both I/O sets in flight: wait for the older run
+  if (c->rh_issued - c->rh_done >= RH_SETS) {  // every I/O set in flight: wait for the oldest run
     pi_status s = rh_wait_one(c);
     if (s != PI_OK) return s;
   }
   const long long run = c->rh_issued;
-  const int k = (int)(run % 2);
+  const int k = (int)(run % RH_SETS);
   const size_t cap = (size_t)c->cfg.capacity;
   float *in = c->io + (size_t)k * 8 * cap, *out = in + 4 * cap;
   const size_t bytes = sizeof(float) * (size_t)n;
@@ -667,7 +669,7 @@ pi_status pi_run_host_submit(pi_ctx c, pi_algo algo, int64_t n, const float *x, 
     e = cudaEventRecord(c->ev_sub, c->stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c->h2d, c->ev_sub, 0);
   }
-  if (e == cudaSuccess && run >= 2) e = cudaStreamWaitEvent(c->h2d, c->ev_binned[k], 0);
+  if (e == cudaSuccess && run >= RH_SETS) e = cudaStreamWaitEvent(c->h2d, c->ev_binned[k], 0);
   for (int a = 0; a < 4 && e == cudaSuccess && n > 0; ++a)
     e = cudaMemcpyAsync(in + a * cap, src[a], bytes, cudaMemcpyHostToDevice, c->h2d);
   if (e == cudaSuccess) e = cudaEventRecord(c->ev_in[k], c->h2d);
@@ -677,7 +679,7 @@ pi_status pi_run_host_submit(pi_ctx c, pi_algo algo, int64_t n, const float *x, 
   if (s != PI_OK) return s;
   e = cudaEventRecord(c->ev_binned[k], c->stream);
   // the output set is free once run-2's results reached the host
-  if (e == cudaSuccess && run >= 2) e = cudaStreamWaitEvent(c->stream, c->ev_done[k], 0);
+  if (e == cudaSuccess && run >= RH_SETS) e = cudaStreamWaitEvent(c->stream, c->ev_done[k], 0);
   if (e != cudaSuccess) return cuda_check(c, e, "pi_run_host_submit");
   s = pi_interact(c, algo, phi ? out : nullptr, fx ? out + cap : nullptr, fy ? out + 2 * cap : nullptr,
                   fz ? out + 3 * cap : nullptr);
