@@ -118,6 +118,16 @@ def traffic_from_profiles(algo):
         return None
 
 
+def smem_from_profiles(algo):
+    """Shared-memory wavefronts of the interaction kernel as a fraction of their peak, from the
+    committed ncu capture (the X-pencil's binding resource), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_smem.json")
+    try:
+        return json.load(open(p)).get(algo)
+    except Exception:
+        return None
+
+
 def oracle_rate(cloud, seconds, threads, rng_seed=7):
     """The fp64 cell-list oracle as it stands, on a bounded random sample of targets."""
     import numpy as np
@@ -445,6 +455,7 @@ def run_ours(a):
         "config": workload_config(a, world, cloud, n_all),
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic_from_profiles(a.algo),
+                     "smem_wavefront_frac_ncu": smem_from_profiles(a.algo),
                      "kernel": f"k_interact_{a.algo}", "flop_per_launch": flop,
                      "flop_model": "8 per candidate + 10 per cutoff pair (SURVEY.md §8(d))",
                      "candidates": C, "cutoff_pairs": P, "kernel_ms": int_ms,
