@@ -1,4 +1,4 @@
-"""Builds profiles/<round>_ncu_summary.md and profiles/ncu_traffic.json from the ncu reports
+"""Builds profiles/<round>_ncu_summary.md, profiles/ncu_traffic.json and ncu_smem.json from the ncu reports
 of tools/profile_round.sh (gpurun_out/<round>_*).  Development aid."""
 import csv, json, os, subprocess, sys
 from collections import defaultdict
@@ -61,7 +61,7 @@ out = [f"# {R}: ncu summaries (B200, `--set full --clock-control none`, one capt
        "Captured by `tools/profile_round.sh` under gpurun; raw reports stay in gpurun_out/ (not tracked).",
        "Durations under ncu are serialised and cold-cache: compare shares, not absolute times (bench.py",
        "times the kernels live with CUDA events).\n"]
-traffic = {}
+traffic, smem = {}, {}
 for name, title in (("xpencil", "X-pencil interaction (configs[1], 2^21, 64^3)"),
                     ("global", "global-memory baseline PPNL (configs[1])"),
                     ("fullload", "full-load interaction (configs[1])")):
@@ -72,6 +72,9 @@ for name, title in (("xpencil", "X-pencil interaction (configs[1], 2^21, 64^3)")
         s, tr = fmt(d)
         out.append(f"## {title}: `{d['Kernel Name'][:60]}`\n{s}\n")
         traffic[name] = int(tr)
+        w = d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")
+        if w not in (None, ""):
+            smem[name] = round(float(w) / 100.0, 4)
 for name, title in (("rebin", "binning, pi_step delta re-binning at 2^24 (configs[2] ppc 8: scan of the carried counts + scatter of the nearly sorted records)"),
                     ("bin", "binning, pi_bin at 2^24 (configs[2] ppc 8, random input order)")):
     rep = os.path.join(G, f"{R}_{name}.ncu-rep")
@@ -100,5 +103,6 @@ if os.path.exists(ll):
         out.append(f"| `{k}` | {cnt[k]} | {v / 1e3:.1f} | {100 * v / s:.1f} % |")
 open(os.path.join(ROOT, "profiles", f"{R}_ncu_summary.md"), "w").write("\n".join(out) + "\n")
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+json.dump(smem, open(os.path.join(ROOT, "profiles", "ncu_smem.json"), "w"), indent=1)
 print("\n".join(out))
 print(traffic)
