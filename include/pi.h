@@ -89,7 +89,8 @@ typedef enum { PI_K_GAUSSIAN = 0, PI_K_INDICATOR = 1, PI_K_CANDIDATE = 2, PI_K_L
  *                  offsets from the global prefix array.
  *   PI_A_XPENCIL : X-pencil (Alg. 5, §5.2), re-designed to stream the
  *                  9 neighbour pencils of a target pencil along X through shared memory.
- *   PI_A_AUTO    : the fastest measured strategy for the workload (currently X-pencil).   */
+ *   PI_A_AUTO    : the fastest measured strategy for the workload: the global-memory kernel
+ *                  below 3 particles per cell (mean), the X-pencil above.                  */
 typedef enum { PI_A_GLOBAL = 0, PI_A_FULLLOAD = 1, PI_A_XPENCIL = 2, PI_A_AUTO = 3 } pi_algo;
 
 typedef struct {

@@ -489,8 +489,18 @@ pi_status pi_bin(pi_ctx c, int64_t n, const float *x, const float *y, const floa
   return PI_OK;
 }
 
+// PI_A_AUTO: the global-memory kernel below ~3 particles per cell (the paper's crossover: the
+// staged kernels pay per-cell overheads with few particles per cell; measured configs[2] ppc 1
+// and 2: 1.5 / 1.9 ms against the X-pencil's 3.8 / 2.2), the X-pencil above
+static pi_algo resolve_auto(pi_ctx c, pi_algo algo) {
+  if (algo != PI_A_AUTO) return algo;
+  const double ppc = (double)c->n / (double)(c->g.ncells > 0 ? c->g.ncells : 1);
+  return ppc < 3.0 ? PI_A_GLOBAL : PI_A_XPENCIL;
+}
+
 static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, float *fy, float *fz, bool integrate,
                              float dt) {
+  algo = resolve_auto(c, algo);
   InteractArgs a{};
   const bool multi = c->cfg.nranks > 1;
   a.n = multi ? c->cfg.capacity : c->n;
@@ -553,6 +563,7 @@ pi_status pi_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, float *fy, 
 
 pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
   if (!c) return PI_EINVAL;
+  algo = resolve_auto(c, algo);
   if (c->state == 0) return fail(c, PI_ESTATE, "pi_step before pi_bin");
   if (!std::isfinite(dt)) return fail(c, PI_EINVAL, "dt must be finite");
   if (c->need_bin) {

@@ -584,8 +584,13 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   p.out = a.out;
   p.ctl = a.ctl;
   const int own = g.own_hi - g.own_lo;
-  p.L = a.tx_len > 0 ? a.tx_len : 64;
-  if (p.L > 128) p.L = 128;
+  // segment length: ~512 targets per item at the mean density (64 cells at 8 per cell, up to
+  // 256 at 2 or fewer), so a slot feeds the consumer warps at low densities too (configs[2]
+  // ppc 1: 7.0 -> 3.8 ms with 256 instead of 64; ppc 4: 2.43 -> 1.88 ms with 128)
+  const double ppc_mean = (double)a.n_est / (double)g.ncells;
+  const int l_auto = ppc_mean >= 8.0 ? 64 : (ppc_mean >= 4.0 ? 128 : 256);
+  p.L = a.tx_len > 0 ? a.tx_len : l_auto;
+  if (p.L > 512) p.L = 512;
   if (p.L > own) p.L = own;
   p.nseg = (own + p.L - 1) / p.L;
   p.nitems = (long long)p.nseg * g.ny * g.nz;
@@ -593,17 +598,21 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   p.sx = g.sx;
   p.mask = k.kernel == PI_K_CANDIDATE || g.nx < 4;
   const int nc = a.threads > 0 ? a.threads / 32 : 20;
-  int cap = a.tx_cap;
-  if (cap <= 0) {
-    // mean occupancy of 9 pencils x (L + 2) cells + 15 %, plus a few records
-    const double ppc = (double)a.n_est / (double)g.ncells;
-    cap = (int)(9.0 * ppc * 1.15 * (p.L + 2) + 64.0);
-  }
-  p.capp = max(16, cap / 2 + 9);  // + one partial pair per run
   p.nslot = a.slots >= 2 ? min(a.slots, MAX_SLOTS) : 2;
   p.dense = a.dense;
   p.tpl = a.tpl == 2 ? 2 : 1;  // default 1: two per lane measured slower
   const size_t max_smem = 227 * 1024;
+  int cap = a.tx_cap;
+  if (cap <= 0) {
+    // every slot as large as shared memory allows (one block per SM either way): rows through
+    // dense regions then need fewer rounds and list fewer cells (clustered configs[3]: -7 %;
+    // measured the same as the mean occupancy + 15 % on uniform input), but no more than the
+    // particles there are
+    const size_t fixed = 128 + (size_t)9 * lf_of(p.L, p.sx) * 4 + (size_t)p.nslot * slot_words(p.L, p.sx) * 4;
+    const long long fit = max_smem > fixed ? (long long)((max_smem - fixed) / ((size_t)p.nslot * 32)) : 16;
+    cap = (int)min(2 * fit - 18, a.n_est + 64);
+  }
+  p.capp = max(16, cap / 2 + 9);  // + one partial pair per run
   while (xp_smem_bytes(p.L, p.capp, p.sx, p.nslot) > max_smem && p.capp > 64) p.capp -= 32;
   if (xp_smem_bytes(p.L, p.capp, p.sx, p.nslot) > max_smem) return cudaErrorNotSupported;
   p.pairs = a.pairs;
