@@ -140,11 +140,13 @@ typedef struct {
 
 /* Tuning knobs of the launch configuration (a5).  Zero fields mean "library default".   */
 typedef struct {
-  int32_t xpencil_len;       /* X-pencil: target cells per work item (row segment) (64)     */
-  int32_t xpencil_cap;       /* X-pencil: records one staging slot holds (9 pencils of the
-                                segment at the mean density + 15 %); a segment that does
-                                not fit is split into rounds, a cell whose window alone does
-                                not fit takes the global-memory path                        */
+  int32_t xpencil_len;       /* X-pencil: target cells per work item (row segment); default
+                                from the mean density: 64 at >= 8 per cell, 128 at >= 4,
+                                256 below                                                   */
+  int32_t xpencil_cap;       /* X-pencil: records one staging slot holds (default: as many as
+                                the shared memory of the block's slots allows); a segment
+                                that does not fit is split into rounds, a cell whose window
+                                alone does not fit is listed for the Par-Cell-SM pass       */
   int32_t fullload_box[3];   /* full load: target sub-box (interior) dims (8, 4, 4)         */
   int32_t fullload_cap;      /* full load: staged particles per block                       */
   int32_t threads;           /* threads per block of the staged kernels                     */
