@@ -128,7 +128,9 @@ typedef struct {
                                 (e.g. a particle moved more than one slab in one step),
                                 8 a pi_bin particle outside this rank's slab                 */
   int64_t candidates;        /* ordered candidate pairs of the last interaction (C)          */
-  int64_t fallback_cells;    /* target cells that took the global-memory fallback            */
+  int64_t fallback_cells;    /* target cells the staged kernels could not stage: computed by
+                                the Par-Cell-SM pass (X-pencil: cells whose window alone
+                                exceeds a slot; full load: the cells of boxes that do not fit) */
   int64_t migrants_in;       /* particles received by the last migration (nranks > 1)       */
   int64_t migrants_out;      /* particles sent by the last migration (nranks > 1)           */
   int64_t steps;             /* pi_step calls so far                                          */
