@@ -2,20 +2,26 @@
 """bench.py -- throughput of the hot path of arXiv 2406.16091 on B200 (driver contract).
 
 A "step" is one pass of the whole hot path over the synthetic cloud of BASELINE.json
-configs[1] (2^21 uniform particles, 64^3 cells, 8 per cell, Gaussian K, r_c = w):
-pi_step = a1-a4 binning (cell index + counts, look-back scan + M_C, scatter), a5-a6
-interaction (X-pencil strategy by default) and a7 position update.  Inputs are resident in
-HBM; L2 is flushed (256 MiB write) between timed steps and the flush is outside the timed
-events.  The metric is candidate pair interactions per second (ordered pairs (i, j), j != i,
-in the 27 neighbour cells -- the unit of the paper's Table 1).
+configs[4] (2^27 uniform particles, 256^3 cells, 8 per cell, Gaussian K, r_c = w -- the
+configuration the metric "pair interactions/s and step ms at 1/2/4/8 B200" is quoted on):
+pi_step = a1-a4 binning (cell index + counts, scan + M_C, scatter), a5-a6 interaction
+(X-pencil strategy by default) and a7 position update.  Inputs are resident in HBM (2 GiB of
+records: larger than L2, and L2 is flushed with a 256 MiB write between timed steps, outside
+the timed events).  The metric is candidate pair interactions per second (ordered pairs (i, j),
+j != i, in the 27 neighbour cells -- the unit of the paper's Table 1).
+configs[1] (2^21, 64^3; round 1's workload) is reported beside it under "config_c1".
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--algo xpencil|global|fullload]
+                  [--scaling strong|weak] [--config c4|c1|...]
   python bench.py --impl reference ...   # the fp64 CPU oracle on a bounded sample (rank 0)
 
-N > 1 (launched with torchrun): the X-slab decomposition (a8) -- rank r owns
-64 X layers of a (64 N) x 64 x 64 grid with 8 particles per cell, so per-GPU work equals the
-N = 1 workload ("scaling": "weak"); each pi_step migrates particles and exchanges ghost
-layers with the X neighbours over NCCL.  Timed on the device, MAX over ranks.
+N > 1 (launched with torchrun): the X-slab decomposition (a8); each pi_step
+migrates particles and exchanges ghost layers with the X neighbours over NCCL.
+  --scaling strong (default): configs[4] itself, 2^27 particles on 256^3 cells split into
+      N X-slabs of 256/N layers ("scaling": "strong").
+  --scaling weak: 2^24 particles per GPU on a (32 N) x 256 x 256 grid (equal to
+      configs[4] at N = 8) ("scaling": "weak").
+Timed on the device, MAX over ranks.
 """
 from __future__ import annotations
 
@@ -32,8 +38,21 @@ sys.path.insert(0, ROOT)
 
 FP32_PEAK_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.45: FMA lanes x SMs x max SM clock
 METRIC = "candidate pair interactions/s (27-cell ordered pairs), step ms"
-WORKLOAD = ("BASELINE configs[1]: 2^21 uniform particles in the unit box, 64^3 cells (8/cell), "
-            "r_c = w = 1/64, Gaussian K sigma = r_c/3, fp32")
+WORKLOADS = {
+    "c4": ("BASELINE configs[4]: 2^27 uniform particles in the unit box, 256^3 cells (8/cell), "
+           "r_c = w = 1/256, Gaussian K sigma = r_c/3, fp32, one B200"),
+    "c1": ("BASELINE configs[1]: 2^21 uniform particles in the unit box, 64^3 cells (8/cell), "
+           "r_c = w = 1/64, Gaussian K sigma = r_c/3, fp32"),
+}
+
+
+def fp32_peak_measured():
+    """The FFMA2 peak measured by tools/pipes.cu on a B200 of this pool (profiles/peaks.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "peaks.json")))
+        return float(d["ffma2_tflops"]), d.get("how", "tools/pipes.cu")
+    except Exception:
+        return None, None
 
 
 def parse():
@@ -42,7 +61,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1")
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--no-c1", action="store_true", help="skip the configs[1] side measurement")
     ap.add_argument("--algo", default="xpencil")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-binning-2e24", action="store_true", help="skip the 2^24 binning measurement")
@@ -157,29 +178,42 @@ def host_cores():
 
 # ------------------------------------------------------------------------ workload (both arms)
 def workload_cloud(a, rank, world):
-    """This rank's synthetic input: configs[1] at N = 1; the X-slab weak-scaling share otherwise."""
+    """This rank's synthetic input: configs[4] (or --config) at N = 1; at N > 1 this rank's X-slab
+    of configs[4] (strong) or of the (32 N) x 256 x 256 weak-scaling grid."""
     import synth
-    if world > 1:
-        # rank r owns 64 X layers of a (64 N) x 64 x 64 grid, 8 uniform particles per cell
-        return synth.slab_uniform(8.0, (64, 64, 64), rank, world, seed=synth.SEED_BASE + 1)
+    if world > 1 or a.scaling == "weak":
+        lx = 32 if a.scaling == "weak" else 256 // world
+        # uniform inside the rank's slab, 8 per cell, w = 1/256 (an independent stream per rank: the
+        # union is a uniform cloud of the same statistics as synth.make_config("c4"))
+        return synth.slab_uniform(8.0, (lx, 256, 256), rank, world, seed=synth.SEED_BASE + 4)
     return synth.make_config(a.config)
 
 
 def workload_config(a, world, cloud, n_total):
     g = cloud.grid
-    if world > 1:
-        workload = (f"X-slab weak scaling: {g.dims[0]}x{g.dims[1]}x{g.dims[2]} cells (64^3 per GPU), 8 uniform "
-                    f"particles per cell (~2^21 per GPU), r_c = w = 1/64, Gaussian K sigma = r_c/3, fp32; NCCL "
-                    "ghost + migration exchange every step")
-    elif a.config == "c1":
-        workload = WORKLOAD
+    if world > 1 or a.scaling == "weak":
+        if a.scaling == "weak":
+            workload = (f"configs[4] weak scaling (SURVEY.md Q22): {g.dims[0]}x{g.dims[1]}x{g.dims[2]} cells, 32 X "
+                        "layers (2^24 uniform particles, 8 per cell) per GPU, r_c = w = 1/256, Gaussian K sigma = r_c/3, "
+                        "fp32; NCCL ghost + migration exchange every step")
+        else:
+            workload = (f"BASELINE configs[4] strong scaling: 2^27 uniform particles, 256^3 cells (8/cell) in {world} "
+                        f"X-slabs of {g.dims[0] // world} layers, r_c = w = 1/256, Gaussian K sigma = r_c/3, fp32; NCCL "
+                        "ghost + migration exchange every step")
+    elif a.config in WORKLOADS:
+        workload = WORKLOADS[a.config]
     else:
         workload = f"synth.make_config({a.config!r}): {cloud.n} particles, {tuple(g.dims)} cells, Gaussian K, fp32"
     return {"workload": workload, "n_per_gpu": cloud.n, "n_total": int(n_total), "cells": g.ncells,
             "algo": a.algo, "step": "pi_step: re-bin (scan of the carried counts + scatter) + interact + integrate"
             + (" + a8 migration/ghost exchange (NCCL)" if world > 1 else ""),
-            "l2": "flushed between timed steps (256 MiB write, outside the events)",
+            "l2": "inputs larger than L2 (2 GiB of records at configs[4]) and L2 flushed between timed steps "
+                  "(256 MiB write, outside the events)",
             "parallelism": f"xslab{world}" if world > 1 else "single GPU"}
+
+
+def scaling_of(a, world):
+    return a.scaling
 
 
 # ------------------------------------------------------------------------ reference arm
@@ -202,7 +236,8 @@ def run_reference(a):
     line = {
         "impl": "reference", "metric": METRIC, "value": value,
         "unit": unit, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": scaling_of(a, world), "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": workload_config(a, world, cloud, cloud.n * world),
         "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "oracle",
                          "sample": f"{info['targets']} random targets of the {cloud.n}-particle cloud per step "
@@ -250,6 +285,39 @@ def binning_at_scale(a, dev, stream, flush):
             "first_bin_ms": f_ms, "first_bin_gbs": byts / (f_ms * 1e-3) / 1e9,
             "first_bin_frac": byts / (f_ms * 1e-3) / 1e9 / peak, "peak_gbs": peak,
             "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy)"}
+
+
+def side_config(a, dev, stream, flush, name):
+    """pi_step of another BASELINE config (device time per step and candidate pairs/s), for
+    continuity with earlier rounds (configs[1] was round 1's bench workload)."""
+    import torch
+    import synth
+    from paper_2406_16091_b200 import Context
+    c = synth.make_config(name)
+    g = c.grid
+    ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=c.n, device=dev, stream=stream)
+    x, y, z, q = (torch.from_numpy(v).to(dev) for v in (c.x, c.y, c.z, c.q))
+    ctx.bin(x, y, z, q)
+    _, fx, fy, fz = ctx.interact(a.algo)
+    dt = 0.01 * g.w / max(float(torch.stack([fx.abs().max(), fy.abs().max(), fz.abs().max()]).max()), 1e-30)
+    del fx, fy, fz
+    for _ in range(3):
+        ctx.step(a.algo, dt)
+    ms, ims, cs = [], [], []
+    for _ in range(10):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.step(a.algo, dt)
+        e1.record(stream)
+        st = ctx.stats()
+        ms.append(e0.elapsed_time(e1))
+        ims.append(st["interact_ms"])
+        cs.append(st["candidates"])
+    ctx.close()
+    m = statistics.median(ms)
+    return {"workload": WORKLOADS.get(name, name), "ms_per_step": m, "value": statistics.mean(cs) / (m * 1e-3),
+            "interact_ms": statistics.median(ims), "unit": "candidate pair interactions/s"}
 
 
 def hbm_peak_gbs():
@@ -350,6 +418,7 @@ def run_ours(a):
     flop = 8.0 * C + 10.0 * P
     int_ms = statistics.mean(inter_ms)
     achieved = flop / (int_ms * 1e-3) / 1e12
+    pk_meas, _ = fp32_peak_measured()
     bin_bytes = 48.0 * n + 12.0 * g.ncells / world
 
     # end to end through the C ABI on pinned host buffers (H2D + bin (+ a8) + interact + D2H).
@@ -361,7 +430,7 @@ def run_ours(a):
     for _ in range(2):
         ctx.run_host(a.algo, hx, hy, hz, hq, *ho)
     e2e_sync = []
-    for _ in range(max(3, a.steps // 2)):
+    for _ in range(max(3, min(a.steps // 2, 6))):
         flush.zero_()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -373,7 +442,7 @@ def run_ours(a):
     e2e_sync_ms = statistics.mean(e2e_sync)
     if world == 1:
         ho2 = [ho] + [[torch.empty(n, dtype=torch.float32).pin_memory() for _ in range(4)] for _ in range(2)]
-        runs = max(6, a.steps)
+        runs = max(6, min(a.steps, 12))
         for k in range(4):
             ctx.run_host_submit(a.algo, hx, hy, hz, hq, *ho2[k % 3])
         ctx.run_host_wait()
@@ -390,16 +459,16 @@ def run_ours(a):
         e2e_path = ("pi_run_host_submit/_wait, 3 runs in flight: pinned H2D x,y,z,q -> bin -> interact -> "
                     "D2H phi,F per run, copies overlapping the previous/next run's kernels")
         # the host link's floor for this run: the same bytes up and down at once, plain copies
-        dev_in = torch.empty(4 * n, dtype=torch.float32, device=dev)
-        dev_out = torch.empty(4 * n, dtype=torch.float32, device=dev)
-        hin = torch.cat([hx, hy, hz, hq]).pin_memory()
-        hout = torch.empty(4 * n, dtype=torch.float32).pin_memory()
+        dev_in = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(4)]
+        dev_out = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(4)]
         su, sd = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         def both():
             with torch.cuda.stream(su):
-                dev_in.copy_(hin, non_blocking=True)
+                for d_, h_ in zip(dev_in, (hx, hy, hz, hq)):
+                    d_.copy_(h_, non_blocking=True)
             with torch.cuda.stream(sd):
-                hout.copy_(dev_out, non_blocking=True)
+                for h_, d_ in zip(ho, dev_out):
+                    h_.copy_(d_, non_blocking=True)
         both()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -413,7 +482,7 @@ def run_ours(a):
         e1.record(stream)
         e1.synchronize()
         link_floor_ms = e0.elapsed_time(e1) / 5
-        del dev_in, dev_out, hin, hout
+        del dev_in, dev_out
     else:
         link_floor_ms = None
         e2e_ms = e2e_sync
@@ -432,13 +501,15 @@ def run_ours(a):
 
     if world > 1:
         # reset, migrate, append, reset, ghosts, append, count, scan, scatter (which writes the
-        # source pairs), interact (+ the full load's Par-Cell-SM kernel); NCCL's own kernels not counted
-        launches = 10 + (1 if a.algo == "fullload" else 0)
+        # source pairs), interact (+ the Par-Cell-SM kernel of the full load and the X-pencil);
+        # NCCL's own kernels not counted
+        launches = 10 + (1 if a.algo in ("fullload", "xpencil") else 0)
     else:
         # pi_step, one rank: scan of the carried counts (k_scan_delta), scatter (which also
         # writes the X-pencil's source pairs), interact (+ integrate fused); plus two memsets of
-        # the control block, not counted.  The full load adds its Par-Cell-SM kernel.
-        launches = 3 + (1 if a.algo == "fullload" else 0)
+        # the control block, not counted.  The full load and the X-pencil add their Par-Cell-SM
+        # kernel (the cells listed for it that no block took during the interaction kernel).
+        launches = 3 + (1 if a.algo in ("fullload", "xpencil") else 0)
     line = {
         "metric": METRIC,
         "value": value,
@@ -448,7 +519,7 @@ def run_ours(a):
         "warmup": a.warmup,
         "ms_per_step": tot_ms / a.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling_of(a, world),
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
@@ -459,7 +530,11 @@ def run_ours(a):
                      "kernel": f"k_interact_{a.algo}", "flop_per_launch": flop,
                      "flop_model": "8 per candidate + 10 per cutoff pair (SURVEY.md §8(d))",
                      "candidates": C, "cutoff_pairs": P, "kernel_ms": int_ms,
-                     "peak_basis": "2 x 128 FP32 lanes x 148 SMs x 1.965 GHz (no FP32 entry in MEASURED_PEAKS)",
+                     "peak_basis": "nominal 2 x 128 FP32 lanes x 148 SMs x 1.965 GHz (MEASURED_PEAKS.json has no "
+                                   "FP32 entry); frac_measured: against the FFMA2 rate measured by tools/pipes.cu "
+                                   "(profiles/peaks.json)",
+                     "peak_measured": pk_meas,
+                     "frac_measured": (achieved / pk_meas) if pk_meas else None,
                      "note": ("effective rate: the unit is the 27-cell candidate pair, but the X-pencil skips "
                               "the X sub-cells farther than r_c from the target (exact; DESIGN.md R18)"
                               if a.algo == "xpencil" else "every 27-cell candidate is evaluated")},
@@ -486,6 +561,8 @@ def run_ours(a):
                                           "cell list incl. its own binning)"}
     if world == 1 and not a.no_binning_2e24:
         line["binning_2e24"] = binning_at_scale(a, dev, stream, flush)
+    if world == 1 and not a.no_c1 and a.config != "c1":
+        line["config_c1"] = side_config(a, dev, stream, flush, "c1")
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -15,7 +15,7 @@
  *          1 INDICATOR c_ij = (q_j, 0, 0, 0) inside the cutoff
  *          2 CANDIDATE c_ij = (q_j, 0, 0, 0) for every candidate pair
  * Outputs per requested target t: out[4] (phi, fx, fy, fz), S[4] = sum |c_ij| over
- * included pairs, A[4] = sum |c_ij| over ambiguous pairs (|r^2 - rc^2| <= band rc^2),
+ * included pairs (Lennard-Jones: per Eq. (1) term, reading R20), A[4] = sum |c_ij| over ambiguous pairs (|r^2 - rc^2| <= band rc^2),
  * C = #candidates, P = #pairs inside the cutoff.  All accumulation in double.
  */
 #include <math.h>
@@ -110,7 +110,7 @@ int oracle_interact(int64_t n, const float *x, const float *y, const float *z, c
             double r2 = ddx * ddx + ddy * ddy + ddz * ddz;
             int inside = r2 < rc2;
             int ambiguous = fabs(r2 - rc2) <= band * rc2;
-            double cij[4];
+            double cij[4], mag[4];
             if (kernel == 0) {
               double K = exp(-r2 * inv2s2);
               double w = (double)q[j] * K;
@@ -130,17 +130,27 @@ int oracle_interact(int64_t n, const float *x, const float *y, const float *z, c
               cij[1] = qi * w * G * ddx;
               cij[2] = qi * w * G * ddy;
               cij[3] = qi * w * G * ddz;
+              /* |c_ij| per Eq. (1) term (reading R20): repulsive and attractive
+                 parts counted separately, so the tolerance does not vanish where they cancel */
+              double Km = 4.0 * lje0 * (s3 * s3 + s3);
+              double Gm = (4.0 * lje0 / (ljr * ljr)) * (12.0 * s3 * s * s + 6.0 * s * s);
+              mag[0] = fabs(w) * Km;
+              mag[1] = fabs(qi * w) * Gm * fabs(ddx);
+              mag[2] = fabs(qi * w) * Gm * fabs(ddy);
+              mag[3] = fabs(qi * w) * Gm * fabs(ddz);
             } else {
               cij[0] = (double)q[j];
               cij[1] = cij[2] = cij[3] = 0.0;
             }
+            if (kernel != 3)
+              for (int m = 0; m < 4; ++m) mag[m] = fabs(cij[m]);
             if (kernel == 2) { inside = 1; ambiguous = 0; }
             if (inside) {
               ++pp;
-              for (int m = 0; m < 4; ++m) { acc[m] += cij[m]; sab[m] += fabs(cij[m]); }
+              for (int m = 0; m < 4; ++m) { acc[m] += cij[m]; sab[m] += mag[m]; }
             }
             if (ambiguous)
-              for (int m = 0; m < 4; ++m) amb[m] += fabs(cij[m]);
+              for (int m = 0; m < 4; ++m) amb[m] += mag[m];
           }
         }
     for (int m = 0; m < 4; ++m) { out[4 * k + m] = acc[m]; S[4 * k + m] = sab[m]; A[4 * k + m] = amb[m]; }

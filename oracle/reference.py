@@ -41,14 +41,25 @@ def lj_terms(r2, r, eps, e0):
     G = -(4.0 * e0 / (r * r)) * (12.0 * s ** 5 - 6.0 * s ** 2)
     return K, G
 
-# Ambiguity band for the cutoff decision (reading R-band): pairs with
-# |r^2 - r_c^2| <= BAND_REL * (w/r_c)^2 * r_c^2 may be included or excluded by an
-# fp32 implementation; their |contribution| is added to A_i (C10).
-BAND_REL = 2.0 ** -17
+
+def lj_term_magnitudes(r2, r, eps, e0):
+    """|contribution| scale of Eq. (1) per term (reading R20: the potential is
+    the sum of the repulsive u^12 and the attractive u^6 term, each a contribution of its own):
+    |K|_terms = 4 E0 (u^12 + u^6) and |G|_terms = (4 E0 / r^2) (12 u^10 + 6 u^4).  They bound the
+    tolerance (C10) of the Lennard-Jones kernel, whose force term vanishes where 12 u^10 = 6 u^4
+    while its two parts do not."""
+    s = (r2 + eps * eps) / (r * r)
+    return 4.0 * e0 * (s ** 6 + s ** 3), (4.0 * e0 / (r * r)) * (12.0 * s ** 5 + 6.0 * s ** 2)
+
+# Ambiguity band for the cutoff decision (SURVEY.md C10, DESIGN.md reading R15): pairs with
+# |r^2 - r_c^2| <= BAND_REL * r_c^2 may be included or excluded by an fp32 implementation;
+# their |contribution| is added to A_i.  An fp32 r^2 from rounded differences is within
+# ~2^-21.7 r^2 of the exact value (tests/test_oracle.py::test_band_covers_fp32_r2 measures it).
+BAND_REL = 2.0 ** -20
 
 
 def band_rel(grid) -> float:
-    return BAND_REL * (float(grid.w) / float(grid.r_c)) ** 2
+    return BAND_REL
 
 
 # ------------------------------------------------------------------------------------
@@ -157,7 +168,8 @@ def candidate_mask(cc_i, cc_j):
 #   LJ:        c_ij = (q_j K, q_i q_j G (x_i - x_j)), K, G of lj_terms (Eq. (1), reading R19)
 #   INDICATOR: c_ij = (q_j, 0, 0, 0) inside the cutoff (test kernel)
 #   CANDIDATE: c_ij = (q_j, 0, 0, 0) for every candidate pair, no cutoff (test kernel)
-# Returned alongside: S_i = sum |c_ij| over included pairs (per component),
+# Returned alongside: S_i = sum |c_ij| over included pairs (per component; for LJ the
+# per-term magnitudes of lj_term_magnitudes, reading R20),
 # A_i = sum |c_ij| over ambiguous pairs (|r^2 - r_c^2| <= band * r_c^2), the candidate
 # count C_i and the cutoff-pair count P_i.  Accumulation in fp64 (C9).
 # ------------------------------------------------------------------------------------
@@ -200,6 +212,10 @@ def brute_force(x, y, z, q, grid, kernel=KERNEL_GAUSSIAN, band=None, chunk=512):
             c0 = Q[None, :] * K
             cf = (Q[s:e, None] * Q[None, :] * G)[:, :, None] * d
             comps = np.concatenate([c0[:, :, None], cf], axis=2)
+            Km, Gm = lj_term_magnitudes(r2, *lj_params(grid))  # reading R20: per-term |c_ij|
+            m0 = np.abs(Q[None, :]) * Km
+            mf = np.abs(Q[s:e, None] * Q[None, :] * Gm)[:, :, None] * np.abs(d)
+            mags = np.concatenate([m0[:, :, None], mf], axis=2)
             incl = inside
         elif kernel == KERNEL_INDICATOR:
             comps = np.zeros(r2.shape + (4,))
@@ -212,9 +228,11 @@ def brute_force(x, y, z, q, grid, kernel=KERNEL_GAUSSIAN, band=None, chunk=512):
             amb = np.zeros_like(amb)
         else:
             raise ValueError(kernel)
+        if kernel != KERNEL_LJ:
+            mags = np.abs(comps)
         out[s:e] = np.einsum("ij,ijk->ik", incl.astype(np.float64), comps)
-        S[s:e] = np.einsum("ij,ijk->ik", incl.astype(np.float64), np.abs(comps))
-        A[s:e] = np.einsum("ij,ijk->ik", amb.astype(np.float64), np.abs(comps))
+        S[s:e] = np.einsum("ij,ijk->ik", incl.astype(np.float64), mags)
+        A[s:e] = np.einsum("ij,ijk->ik", amb.astype(np.float64), mags)
         C[s:e] = cand.sum(axis=1)
         P[s:e] = inside.sum(axis=1)
     return dict(out=out, S=S, A=A, C=C, P=P)

@@ -223,6 +223,13 @@ static bool config_ok(const pi_config *cfg, char *why, size_t n) {
   if (cfg->nranks > 1 && !cfg->nccl_unique_id) { snprintf(why, n, "nranks > 1 needs nccl_unique_id"); return false; }
   long long nc = (long long)cfg->dims[0] * cfg->dims[1] * cfg->dims[2];
   if (nc > (1LL << 30)) { snprintf(why, n, "too many cells"); return false; }
+  // the fine (X sub-cell) index is 32-bit arithmetic in the kernels; with nranks > 1
+  // the local grid has two extra X layers
+  const long long lx = cfg->dims[0] / cfg->nranks + (cfg->nranks > 1 ? 2 : 0);
+  if (lx * cfg->dims[1] * cfg->dims[2] * (cfg->x_subcells > 0 ? cfg->x_subcells : 2) >= (1LL << 31) - 1) {
+    snprintf(why, n, "cells x x_subcells must stay below 2^31");
+    return false;
+  }
   return true;
 }
 
@@ -522,6 +529,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.out.sid = c->sid;
   a.out.uid = c->uid;
   a.out.dt = dt;
+  a.out.flags = &c->ctl->flags;
   if (integrate && c->pcounts_ok) {  // movers update the persistent counts and their tile sums
     a.out.pcounts = c->pcounts;
     a.out.ptsum = c->ptsum;
@@ -600,10 +608,16 @@ pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
   return PI_OK;
 }
 
+static pi_status rh_wait_all(pi_ctx c);
+
 pi_status pi_run_host(pi_ctx c, pi_algo algo, int64_t n, const float *x, const float *y, const float *z,
                       const float *q, float *phi, float *fx, float *fy, float *fz) {
   if (!c) return PI_EINVAL;
   if (n < 0 || n > c->cfg.capacity) return fail(c, PI_ECAPACITY, "n out of range");
+  {  // it uses I/O set 0, which pipelined runs in flight may still read or write
+    pi_status s = rh_wait_all(c);
+    if (s != PI_OK) return s;
+  }
   if (n > 0 && (!x || !y || !z || !q)) return fail(c, PI_EINVAL, "NULL host input");
   size_t cap = (size_t)c->cfg.capacity;
   float *dx = c->io, *dy = c->io + cap, *dz = c->io + 2 * cap, *dq = c->io + 3 * cap;
@@ -640,6 +654,14 @@ static pi_status rh_wait_one(pi_ctx c) {
   if (e == cudaSuccess) e = cudaStreamWaitEvent(c->stream, c->ev_done[k], 0);
   ++c->rh_done;
   return cuda_check(c, e, "pi_run_host_wait");
+}
+
+static pi_status rh_wait_all(pi_ctx c) {
+  while (c->rh_done < c->rh_issued) {
+    pi_status s = rh_wait_one(c);
+    if (s != PI_OK) return s;
+  }
+  return PI_OK;
 }
 
 pi_status pi_run_host_submit(pi_ctx c, pi_algo algo, int64_t n, const float *x, const float *y, const float *z,

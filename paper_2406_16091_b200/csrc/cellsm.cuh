@@ -151,40 +151,40 @@ __device__ void cs_targets(const CsParams &p, int t0, int tbase, int nt, int P, 
   }
 }
 
-// The dense-cell phase: every thread of the block (NT of them) runs it after the block's
-// X-pencil work.  Cells are listed by the producers of all blocks while the phase may already
-// run, so a ticket beyond the current count waits until either the cell is listed or every
-// block's producer has finished (ctl->pad[2] == gridDim.x).  An entry is published by its value
-// (entries are -1 when free: a reader spins on its entry, then frees it for the next launch).
+// The dense-cell phase: every thread of the block (NT of them) runs it.  A block claims listed
+// cells one at a time (compare-and-swap on the ticket counter, so a ticket is only ever taken
+// for a cell already counted in the list) and leaves as soon as no listed cell is left: it never
+// waits for other blocks, so there is no assumption that the whole grid is resident (ADVICE r01:
+// the X-pencil blocks used to wait for every block's producer, which can deadlock when grids of
+// concurrent launches share the GPU).  The X-pencil runs the phase opportunistically after its
+// own items; the cells listed after a block left are computed by k_cellsm_list, launched after
+// the X-pencil kernel (the list is final then).  An entry is published by its value (entries are
+// -1 when free: a reader waits for its reserved entry -- the producer that reserved it is running
+// and writes it next -- then frees it for the next launch).
 template <int KERNEL, bool UPD, int NT>
-__device__ void cellsm_phase(const CsParams &p, unsigned char *smem, bool wait_producers) {
+__device__ void cellsm_phase(const CsParams &p, unsigned char *smem) {
   float4 *A = reinterpret_cast<float4 *>(smem), *B = A + CS_CHUNK;
   int *rstart = reinterpret_cast<int *>(A + 2 * CS_CHUNK);  // [10]
   int *rpa = rstart + 10, *ra = rpa + 9, *rb = ra + 9;      // [9] each
   int *s_sh = rb + 9;                                        // item, n, cell
   const int tid = threadIdx.x;
   const Geom &g = p.g;
-  volatile unsigned long long *cnt = &p.ctl->pad[0], *done = &p.ctl->pad[2];
+  volatile unsigned long long *cnt = &p.ctl->pad[0], *tick = &p.ctl->pad[1];
   volatile int *list = p.list;
   for (;;) {
     __syncthreads();  // the previous cell's shared tables are no longer read
     if (tid == 0) {
-      const long long t = (long long)atomicAdd(&p.ctl->pad[1], 1ull);
+      long long t = -1;
       int cell = -1;
-      unsigned ns = 32;
       for (;;) {
-        if ((unsigned long long)t < *cnt) {  // reserved: wait for its value
+        const unsigned long long tk = *tick;
+        if (tk >= *cnt) break;  // nothing listed left
+        if (atomicCAS(&p.ctl->pad[1], tk, tk + 1) == tk) {
+          t = (long long)tk;
           while ((cell = list[t]) < 0) __nanosleep(32);
           list[t] = -1;
           break;
         }
-        if (!wait_producers || *done >= gridDim.x) {
-          __threadfence();
-          if ((unsigned long long)t < *cnt) continue;
-          break;  // every producer finished and the list is exhausted
-        }
-        __nanosleep(ns);
-        ns = ns < 1024 ? 2 * ns : 1024;
       }
       s_sh[2] = cell;
       s_sh[0] = (int)t;
@@ -236,7 +236,7 @@ __device__ void cellsm_phase(const CsParams &p, unsigned char *smem, bool wait_p
 template <int KERNEL, bool UPD>
 __global__ void __launch_bounds__(256) k_cellsm_list(CsParams p) {
   extern __shared__ __align__(16) unsigned char cs_raw[];
-  cellsm_phase<KERNEL, UPD, 256>(p, cs_raw, false);
+  cellsm_phase<KERNEL, UPD, 256>(p, cs_raw);
 }
 
 }  // namespace pi

@@ -335,8 +335,6 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
           if (lane == 0) {
             sl.meta[0] = 1;
             mbar_arrive(&full[s]);
-            __threadfence();  // this block's listed cells precede its "producer done"
-            atomicAdd(&p.ctl->pad[2], 1ull);
           }
           break;
         }
@@ -505,8 +503,8 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     }
   }
 
-  // the dense cells listed by the producers of all blocks (Par-Cell-SM, cellsm.cuh), in the
-  // staging memory this block no longer uses
+  // the dense cells listed so far by the producers of all blocks (Par-Cell-SM, cellsm.cuh), in
+  // the staging memory this block no longer uses; the rest is left to k_cellsm_list
   __syncthreads();
   {
     CsParams cp;
@@ -520,7 +518,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     cp.out = p.out;
     cp.ctl = p.ctl;
     cp.from_rec = false;
-    cellsm_phase<KERNEL, UPD, (NC + 1) * 32>(cp, slots, true);
+    cellsm_phase<KERNEL, UPD, (NC + 1) * 32>(cp, slots);
   }
 
   // statistics: warp-level sums, spread over CAND_SLOTS counters
@@ -572,6 +570,38 @@ cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
   }
 }
 
+// the cells listed for Par-Cell-SM that no X-pencil block took before it left (cellsm.cuh)
+cudaError_t launch_dense_rest(const XpParams &p, cudaStream_t s) {
+  CsParams cp;
+  cp.rec = p.rec;
+  cp.pairs = p.pairs;
+  cp.plane = p.plane;
+  cp.offsets = p.offsets;
+  cp.list = p.dense;
+  cp.g = p.g;
+  cp.kp = p.kp;
+  cp.out = p.out;
+  cp.ctl = p.ctl;
+  cp.from_rec = false;
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = allow_max_smem(kern);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, CS_SMEM);
+    kern<<<sms * (occ > 0 ? occ : 1), 256, CS_SMEM, s>>>(cp);
+    return cudaGetLastError();
+  };
+  const bool upd = p.out.upd != nullptr;
+  switch (p.kp.kernel) {
+    case PI_K_GAUSSIAN: return upd ? go(k_cellsm_list<PI_K_GAUSSIAN, true>) : go(k_cellsm_list<PI_K_GAUSSIAN, false>);
+    case PI_K_INDICATOR: return upd ? go(k_cellsm_list<PI_K_INDICATOR, true>) : go(k_cellsm_list<PI_K_INDICATOR, false>);
+    case PI_K_LJ: return upd ? go(k_cellsm_list<PI_K_LJ, true>) : go(k_cellsm_list<PI_K_LJ, false>);
+    default: return upd ? go(k_cellsm_list<PI_K_CANDIDATE, true>) : go(k_cellsm_list<PI_K_CANDIDATE, false>);
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s) {
@@ -602,13 +632,24 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   p.dense = a.dense;
   p.tpl = a.tpl == 2 ? 2 : 1;  // default 1: two per lane measured slower
   const size_t max_smem = 227 * 1024;
+  // the segment must leave room for slots of a useful size: the fixed tables (offsets per X
+  // sub-cell boundary of every slot and of the prefetch stage) grow with L * sx (ADVICE r01:
+  // L = 256 with sx = 16 did not fit at all).  Halve L until two slots hold the windows of a
+  // few cells at the mean density.
+  auto fixed_of = [&](int L) {
+    return 128 + (size_t)9 * lf_of(L, p.sx) * 4 + (size_t)p.nslot * slot_words(L, p.sx) * 4;
+  };
+  const size_t min_slot = (size_t)(9 * 8 * (ppc_mean + 4.0)) * 16 + 1024;  // ~8 cells' windows
+  while (p.L > 8 && fixed_of(p.L) + (size_t)p.nslot * min_slot > max_smem) p.L = (p.L + 1) / 2;
+  p.nseg = (own + p.L - 1) / p.L;
+  p.nitems = (long long)p.nseg * g.ny * g.nz;
   int cap = a.tx_cap;
   if (cap <= 0) {
     // every slot as large as shared memory allows (one block per SM either way): rows through
     // dense regions then need fewer rounds and list fewer cells (clustered configs[3]: -7 %;
     // measured the same as the mean occupancy + 15 % on uniform input), but no more than the
     // particles there are
-    const size_t fixed = 128 + (size_t)9 * lf_of(p.L, p.sx) * 4 + (size_t)p.nslot * slot_words(p.L, p.sx) * 4;
+    const size_t fixed = fixed_of(p.L);
     const long long fit = max_smem > fixed ? (long long)((max_smem - fixed) / ((size_t)p.nslot * 32)) : 16;
     cap = (int)min(2 * fit - 18, a.n_est + 64);
   }
@@ -624,9 +665,9 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  if (nc <= 8) return launch_nc<8>(p, s);
-  if (nc <= 16) return launch_nc<16>(p, s);
-  return launch_nc<20>(p, s);
+  cudaError_t e = nc <= 8 ? launch_nc<8>(p, s) : (nc <= 16 ? launch_nc<16>(p, s) : launch_nc<20>(p, s));
+  if (e != cudaSuccess) return e;
+  return launch_dense_rest(p, s);
 }
 
 }  // namespace pi

@@ -151,6 +151,7 @@ struct OutDesc {
   // changes in the update moves one count from its old to its new fine cell
   int32_t *pcounts;
   int32_t *ptsum;          // their per-scan-tile sums (kept current with them)
+  int *flags;              // the context's sticky device flags (DevCtl::flags)
 };
 
 // UPD = false compiles the pi_step update out (kernels specialised for pi_interact).
@@ -174,6 +175,11 @@ __device__ __forceinline__ void write_output(const OutDesc &o, const Geom &g, in
     u.y = integrate1(rec.y, fy, o.dt, g.ly, g.hy);
     u.z = integrate1(rec.z, fz, o.dt, g.lz, g.hz);
     u.w = rec.w;
+    // a non-finite update (NaN / inf force) would be clamped onto the lower wall by integrate1:
+    // raise the sticky out-of-box / NaN flag instead of moving it silently
+    if (!(isfinite(fmaf(o.dt, fx, rec.x)) && isfinite(fmaf(o.dt, fy, rec.y)) && isfinite(fmaf(o.dt, fz, rec.z))) &&
+        o.flags)
+      atomicOr(o.flags, FLAG_OUT_OF_BOX);
     o.upd[t] = u;
     o.uid[t] = o.sid[t];
     if (o.pcounts) {

@@ -14,8 +14,7 @@ from tests._util import assert_parity, ctx_for, gpu_interact, oracle_interact, t
 pytestmark = pytest.mark.gpu
 ALGOS = ["global", "xpencil", "fullload"]
 # Every strategy computes r^2 from differences of the raw fp32 positions: for dyadic inputs
-# every step is exact, so pairs at exactly r = r_c are excluded exactly (band 0).
-EXACT_BOUNDARY = {"global": True, "xpencil": True, "fullload": True}
+# every step is exact, so pairs at exactly r = r_c are excluded exactly (band 0) by all of them.
 
 
 @pytest.mark.parametrize("algo", ALGOS)
@@ -49,20 +48,17 @@ def test_hand2x3_exact(algo, variant):
     """C12: dyadic coordinates; variant B has pairs at exactly r = r_c that must be excluded."""
     import json, os
     g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hand2x3.json")))
-    exact = EXACT_BOUNDARY[algo] or variant == "A"   # variant B has pairs at exactly r_c
-    band = 0.0 if exact else None
+    band = 0.0   # variant B has pairs at exactly r_c: excluded exactly
     c = synth.hand_2x3(variant)
     c.q = np.ones(9, np.float32)
     got, _ = gpu_interact(c, algo, "candidate")
     assert got[:, 0].tolist() == g["candidate_q1"]
     got, _ = gpu_interact(c, algo, "indicator")
-    if exact:
-        assert got[:, 0].tolist() == g["indicator_q1"]
+    assert got[:, 0].tolist() == g["indicator_q1"]
     assert_parity(got, oracle_interact(c, "indicator", band=band), label="hand indicator")
     c = synth.hand_2x3(variant)
     got, _ = gpu_interact(c, algo, "indicator")
-    if exact:
-        assert got[:, 0].tolist() == g["indicator_qj"]
+    assert got[:, 0].tolist() == g["indicator_qj"]
     want = oracle_interact(c, "gaussian", band=band)
     got, _ = gpu_interact(c, algo, "gaussian")
     assert_parity(got, want, label="hand gaussian")
@@ -73,11 +69,10 @@ def test_hand2x3_exact(algo, variant):
 def test_lattice_exact_boundary(algo, d):
     """C14: dyadic lattice with pairs at exactly r = r_c (band 0): interior phi/q closed form."""
     c = synth.lattice(d)
-    band = 0.0 if EXACT_BOUNDARY[algo] else None
+    band = 0.0
     got, _ = gpu_interact(c, algo, "indicator")
     want = oracle_interact(c, "indicator", band=band)
-    if EXACT_BOUNDARY[algo]:
-        assert np.array_equal(got[:, 0], want["P"].astype(np.float64))
+    assert np.array_equal(got[:, 0], want["P"].astype(np.float64))
     assert_parity(got, want, label=f"lattice{d} {algo} indicator")
     got, _ = gpu_interact(c, algo, "gaussian")
     want = oracle_interact(c, "gaussian", band=band)
@@ -255,12 +250,9 @@ def test_run_host_paths(algo):
         assert_parity(torch.stack(hout[k], 1).numpy(), wants[k], label=f"run_host_submit {algo} run {k}")
 
 
-# (Lennard-Jones is left out here: on this clustered cloud one particle's force is dominated by
-# a single pair near the LJ force zero, 12 s^5 = 6 s^2, where the fp32 term itself cancels to
-# ~1e-4 relative -- all three strategies agree on it to 1e-7, the fp64 oracle does not, and the
-# per-particle bound 1e-4 sum|c_ij| (R14) has no room for cancellation inside one term.  The LJ
-# path of the Par-Cell-SM pass is checked on uniform input in test_gpu_step.)
-@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate"])
+# Lennard-Jones included: its tolerance scale is per Eq. (1) term (reading R20), so a pair near
+# the zero of the LJ force (12 u^10 = 6 u^4), where the fp32 term cancels, is covered.
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate", "lj"])
 @pytest.mark.parametrize("xcap", [16, 200])
 def test_dense_cells_par_cell_sm(kernel, xcap):
     """Cells whose window alone does not fit an X-pencil slot are listed and computed by the
@@ -284,19 +276,46 @@ def test_full_size_sampled(name):
     sampled targets against the oracle: configs[3] clustered (M_C ~ 370: the X-pencil lists its
     densest cells for the Par-Cell-SM pass) and the two ends of the configs[2] ppc sweep (1 and
     64 per cell).  Candidates are checked against the oracle's count on the sample's cells'
-    closed form at full size: sum over cells of n_c (sum of the 27 neighbours' counts) - N."""
+    closed form at full size, from the ORACLE's own binning: sum over cells of n_c (sum of the 27
+    neighbours' counts) - N."""
     c = synth.make_config(name)
     ctx = ctx_for(c)
     got, ctx = gpu_interact(c, "xpencil", ctx=ctx)
     sample = np.random.default_rng(5).choice(c.n, 4000, replace=False)
     want = oracle_interact(c, targets=sample)
     assert_parity(got[sample], want, label=f"{name} xpencil")
-    counts, _ = (t.cpu().numpy().astype(np.int64) for t in ctx.get_offsets())
+    assert ctx.stats()["candidates"] == oracle_candidates(c)
+    if name == "c3":
+        assert ctx.stats()["fallback_cells"] > 0
+
+
+def oracle_candidates(c):
+    """C = sum_c n_c (sum of the 27 clamped neighbours' counts) - N from the oracle's binning."""
+    counts = ref.counts_of(celllist.cells(c.x, c.y, c.z, c.grid), c.grid.ncells)
     nx, ny, nz = c.grid.dims
     n3 = counts.reshape(nz, ny, nx)
     pad = np.pad(n3, 1)
     nb = sum(pad[1 + dz:1 + dz + nz, 1 + dy:1 + dy + ny, 1 + dx:1 + dx + nx]
              for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1))
-    assert ctx.stats()["candidates"] == int((n3 * nb).sum() - c.n)
-    if name == "c3":
-        assert ctx.stats()["fallback_cells"] > 0
+    return int((n3 * nb).sum() - c.n)
+
+
+@pytest.mark.parametrize("algo", ["global", "fullload"])
+def test_full_size_other_strategies(algo):
+    """The global baseline and the full load at full size: configs[2] ppc 8 (2^24 on 128^3),
+    sampled targets against the oracle, candidates against the oracle's closed form."""
+    c = synth.make_config("c2_ppc8")
+    got, ctx = gpu_interact(c, algo)
+    sample = np.random.default_rng(6).choice(c.n, 4000, replace=False)
+    assert_parity(got[sample], oracle_interact(c, targets=sample), label=f"c2_ppc8 {algo}")
+    assert ctx.stats()["candidates"] == oracle_candidates(c)
+
+
+def test_c4_full_size_sampled():
+    """configs[4] on one GPU (2^27 uniform, 256^3 cells: the bench's workload) with the bench's
+    strategy: sampled targets against the oracle, candidates against its closed form."""
+    c = synth.make_config("c4")
+    got, ctx = gpu_interact(c, "xpencil")
+    sample = np.random.default_rng(7).choice(c.n, 3000, replace=False)
+    assert_parity(got[sample], oracle_interact(c, targets=sample), label="c4 xpencil")
+    assert ctx.stats()["candidates"] == oracle_candidates(c)

@@ -89,3 +89,40 @@ def test_step_capturable_in_cuda_graph():
     assert np.array_equal(a["id"][oa], b["id"][ob])
     for key in ("x", "y", "z"):  # same arithmetic; within-cell order (atomics) may differ
         assert np.allclose(a[key][oa], b[key][ob], rtol=0, atol=1e-6)
+
+
+@pytest.mark.parametrize("name,steps", [("c1", 3), ("c4", 2)])
+def test_step_full_size_sampled(name, steps):
+    """pi_step in the bench's configuration (the X-pencil, default tuning, the carried-count
+    re-binning of the nearly sorted records, the fused update) at configs[1] (2^21, 64^3) and
+    configs[4] (2^27, 256^3): after warm-up steps, one step's forces on sampled particles against
+    the oracle at the GPU's pre-step state (C11), the update against x + dt F, and the following
+    re-binning bit-exact per cell against the oracle's binning of the updated positions."""
+    c = synth.make_config(name)
+    g = c.grid
+    ctx = ctx_for(c)
+    ctx.bin(*to_dev(c))
+    _, fx, fy, fz = ctx.interact("xpencil")
+    fmax = float(torch.stack([fx.abs().max(), fy.abs().max(), fz.abs().max()]).max())
+    dt = float(np.float32(0.01 * g.w / fmax))   # max |dx| = 1 % of a cell per step (SURVEY §8(d))
+    for _ in range(steps):
+        ctx.step("xpencil", dt)
+    s0 = state(ctx)
+    ctx.step("xpencil", dt)
+    s1 = state(ctx)
+    order0, order1 = np.argsort(s0["id"]), np.argsort(s1["id"])
+    assert np.array_equal(s0["id"][order0], s1["id"][order1])
+    X0 = [s0[k][order0] for k in ("x", "y", "z", "q")]
+    sample = np.random.default_rng(11).choice(c.n, 3000, replace=False)
+    want = celllist.interact(*X0, g, targets=sample)
+    got = np.stack([s1[k][order1][sample] for k in ("phi", "fx", "fy", "fz")], 1).astype(np.float64)
+    assert_parity(got, want, label=f"{name} step forces")
+    for ax, a in (("x", 1), ("y", 2), ("z", 3)):
+        exp = ref.integrate(X0["xyz".index(ax)][sample], got[:, a], dt, 0.0, 1.0)
+        assert np.allclose(s1[ax][order1][sample], exp, rtol=0, atol=2e-7 + 1e-6 * dt)
+    moved = np.mean(celllist.cells(s1["x"], s1["y"], s1["z"], g) != celllist.cells(s0["x"], s0["y"], s0["z"], g))
+    assert moved > 0   # the step moved particles across cells: the re-binning below is exercised
+    ctx.step("xpencil", dt)    # re-bins s1's positions before interacting
+    counts, offsets = (t.cpu().numpy() for t in ctx.get_offsets())
+    wc, wo, _ = celllist.binning(celllist.cells(s1["x"], s1["y"], s1["z"], g), g.ncells)
+    assert np.array_equal(counts, wc) and np.array_equal(offsets, wo)

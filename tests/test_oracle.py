@@ -432,3 +432,116 @@ def test_integrate_reflection():
     x = ref.integrate([0.1, 0.9, 0.5], [-3.0, 2.0, 1.0], 0.05, 0.0, 1.0)
     assert np.allclose(x, [0.05, 1.0, 0.55]) and x[1] < 1.0
     assert np.allclose(ref.integrate([0.9], [4.0], 0.05, 0.0, 1.0), [0.9])
+
+
+# ---------------------------------------------------------------- the acceptance check itself (C10)
+# check_interactions gates every floating-point parity test; these pin that it REJECTS wrong
+# answers (a checker that always passed would turn every GPU parity test green).
+
+def _c0_reference(kernel=ref.KERNEL_GAUSSIAN):
+    c = synth.make_config("c0")
+    return c, celllist.interact(c.x, c.y, c.z, c.q, c.grid, kernel=kernel)
+
+
+def test_check_accepts_oracle_and_small_error():
+    _, r = _c0_reference()
+    ok, worst, _ = ref.check_interactions(r["out"].copy(), r)
+    assert ok and worst == 0.0
+    got = r["out"] + 0.5e-4 * r["S"] * np.where(np.arange(r["out"].size).reshape(r["out"].shape) % 2, 1, -1)
+    ok, worst, _ = ref.check_interactions(got, r)
+    assert ok and 0.49 <= worst <= 0.51
+
+
+def test_check_rejects_relative_error_above_bound():
+    _, r = _c0_reference()
+    i = int(np.argmax(r["S"][:, 2]))
+    got = r["out"].copy()
+    got[i, 2] += 2e-4 * r["S"][i, 2]          # one component of one particle, 2x the bound
+    ok, worst, where = ref.check_interactions(got, r)
+    assert not ok and tuple(where) == (i, 2) and worst == pytest.approx(2.0, rel=1e-6)
+
+
+def test_check_rejects_flipped_force_sign():
+    _, r = _c0_reference()
+    # a particle whose force component is not negligible against its bound
+    cand = np.nonzero(np.abs(r["out"][:, 1]) > 1e-3 * r["S"][:, 1])[0]
+    i = int(cand[0])
+    got = r["out"].copy()
+    got[i, 1] = -got[i, 1]
+    ok, _, where = ref.check_interactions(got, r)
+    assert not ok and tuple(where) == (i, 1)
+
+
+def test_check_rejects_nonzero_where_nothing_contributes():
+    c, r = _c0_reference()
+    iso = np.nonzero((r["S"][:, 0] == 0) & (r["A"][:, 0] == 0))[0]
+    assert len(iso) > 0  # configs[0] has isolated particles (1 per cell on average)
+    got = r["out"].copy()
+    got[iso[0], 0] = 1e-30
+    ok, worst, where = ref.check_interactions(got, r)
+    assert not ok and worst == np.inf and tuple(where) == (iso[0], 0)
+
+
+def test_check_rejects_nan_and_dropped_term():
+    c, r = _c0_reference()
+    got = r["out"].copy()
+    got[5, 3] = np.nan
+    assert not ref.check_interactions(got, r)[0]
+    # drop the largest contribution of one particle (a plausible kernel bug: a skipped source)
+    i = int(np.argmax(r["P"]))
+    one = ref.brute_force(c.x, c.y, c.z, c.q, c.grid)
+    assert np.allclose(one["out"], r["out"], rtol=1e-12, atol=1e-15)
+    X = np.stack([c.x, c.y, c.z], 1).astype(np.float64)
+    d2 = ((X - X[i]) ** 2).sum(1)
+    d2[i] = np.inf
+    j = int(np.argmin(d2))
+    s = float(np.float32(c.grid.sig))
+    got = r["out"].copy()
+    got[i, 0] -= float(c.q[j]) * math.exp(-d2[j] / (2 * s * s))
+    assert not ref.check_interactions(got, r)[0]
+
+
+def test_band_covers_fp32_r2():
+    """The ambiguity band (C10, 2^-20 r_c^2) against the fp32 evaluation every kernel uses:
+    d = fl(x_s - x_t) per axis, r2 = fl(dx dx), fma(dy, dy, r2), fma(dz, dz, r2) (one rounding
+    each; an fma is emulated exactly in fp64 then rounded).  Measured over 10^6 pairs sampled near
+    r = r_c anywhere in the unit box (small coordinates included, where the differences are not
+    exact): the worst |r2_fp32 - r2| / r_c^2 stays below half the band."""
+    rng = np.random.default_rng(2406)
+    f32 = np.float32
+    worst = 0.0
+    for rc in (1 / 16, 1 / 64, 1 / 256, 0.1):
+        n = 250_000
+        xt = rng.random((n, 3)).astype(f32)
+        xt[: n // 4] *= f32(1e-2)  # near the origin: inexact differences
+        u = rng.normal(size=(n, 3))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        r = rc * (1 + rng.uniform(-1e-5, 1e-5, n))
+        xs = (xt.astype(np.float64) + u * r[:, None]).astype(f32)
+        d = (xs - xt).astype(f32)                      # fl32(x_s - x_t)
+        r2 = (d[:, 0] * d[:, 0]).astype(f32)
+        r2 = (d[:, 1].astype(np.float64) ** 2 + r2.astype(np.float64)).astype(f32)
+        r2 = (d[:, 2].astype(np.float64) ** 2 + r2.astype(np.float64)).astype(f32)
+        exact = ((xs.astype(np.float64) - xt.astype(np.float64)) ** 2).sum(1)
+        rc2 = float(f32(rc)) ** 2
+        worst = max(worst, float(np.max(np.abs(r2.astype(np.float64) - exact)) / rc2))
+    assert worst <= 0.5 * ref.BAND_REL, worst
+
+
+def test_lj_term_magnitudes_hand_values():
+    """Reading R20: the LJ tolerance scale is the sum of the magnitudes of Eq. (1)'s two terms.
+    At u^2 = 1/4 (r = 1, eps = 0, E0 = 1, d = 1/2): |K| terms = 4 (1/4096 + 1/64) = 260/4096,
+    |G| terms = 4 (12/1024 + 6/16) = 99/64, so S_0 = q1 260/4096 and S_0x = q0 q1 (99/64)(1/2).
+    At the zero of the LJ force (12 u^10 = 6 u^4) the scale stays 2 * 6 u^4 * 4 E0 / r^2."""
+    grid = synth.Grid(dims=(2, 2, 2), w=1.0, lj_r=1.0, lj_eps=0.0, lj_e0=1.0)
+    f = np.float32
+    x, y, z = np.array([0.25, 0.75], f), np.array([0.5, 0.5], f), np.array([0.5, 0.5], f)
+    q = np.array([1.5, 0.5], f)
+    for r in (ref.brute_force(x, y, z, q, grid, kernel=ref.KERNEL_LJ),
+              celllist.interact(x, y, z, q, grid, kernel=ref.KERNEL_LJ)):
+        assert r["S"][0, 0] == 0.5 * 260.0 / 4096.0 and r["S"][1, 0] == 1.5 * 260.0 / 4096.0
+        assert r["S"][0, 1] == 1.5 * 0.5 * (99.0 / 64.0) * 0.5 and np.all(r["S"][:, 2:] == 0)
+    u2 = 0.5 ** (1 / 3)  # u^6 = 1/2: the force term cancels
+    Km, Gm = ref.lj_term_magnitudes(u2, 1.0, 0.0, 1.0)
+    K, G = ref.lj_terms(u2, 1.0, 0.0, 1.0)
+    assert abs(G) < 1e-12 and Gm == pytest.approx(4 * 12 * u2 ** 2, rel=1e-12)

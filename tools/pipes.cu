@@ -65,24 +65,31 @@ __global__ void k_mix(float *out, float b, float c, long long *cyc) {
 }
 int main(){
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  float *out; long long *cyc; cudaMalloc(&out, sizeof(float)*sms*8*256); cudaMalloc(&cyc, 8);
-  struct { const char* name; void(*k)(float*,float,float,long long*); double ops; } tests[] = {
-    {"FFMA  (lane-FMA/clk/SM)", k_ffma, 8.0*ITERS}, {"FFMA2 (lane-FMA/clk/SM)", k_ffma2, 16.0*ITERS},
-    {"MUFU.EX2 (ex2/clk/SM)", k_ex2, 8.0*ITERS}, {"MIX (candidates/clk/SM)", k_mix, 2.0*ITERS}};
-  for (auto &t : tests) for (int occ : {8, 16}) {
-    int blocks = sms*occ/8*1, threads = 256;  // occ warps per SMSP-ish
-    blocks = sms * occ / 2;
-    for (int rep=0; rep<2; ++rep){
-      cudaMemset(cyc,0,8); cudaEvent_t a,b; cudaEventCreate(&a); cudaEventCreate(&b);
-      cudaEventRecord(a); t.k<<<blocks,threads>>>(out,0.999f,1e-4f,cyc); cudaEventRecord(b); cudaEventSynchronize(b);
-      float ms; cudaEventElapsedTime(&ms,a,b); long long c; cudaMemcpy(&c,cyc,8,cudaMemcpyDeviceToHost);
-      double total = t.ops * (double)blocks * threads;
-      double per_sm_clk = total / ((double)c * sms) * ((double)blocks / (sms * (double)(occ/2 > 0 ? 1 : 1)));
-      // blocks are co-resident when blocks <= sms*8 (256 thr, <=2048 thr/SM): use max cycles of one block
-      int resident = blocks / sms; // blocks per SM (all resident)
-      double rate = t.ops * threads * resident / (double)c;
-      if (rep) printf("%-28s blocks/SM=%2d  %8.2f per clk per SM   (%.3f ms, %lld cyc)\n", t.name, resident, rate, ms, c);
+  float *out; long long *cyc; cudaMalloc(&out, sizeof(float)*sms*16*256); cudaMalloc(&cyc, 8);
+  // ops per thread: FFMA / FFMA2 count lane-FMAs (2 FLOP each), EX2 counts ex2, MIX candidates
+  struct { const char* name; const char* key; void(*k)(float*,float,float,long long*); double ops; double flop_per_op; } tests[] = {
+    {"FFMA  (lane-FMA/clk/SM)", "ffma", k_ffma, 8.0*ITERS, 2.0}, {"FFMA2 (lane-FMA/clk/SM)", "ffma2", k_ffma2, 16.0*ITERS, 2.0},
+    {"MUFU.EX2 (ex2/clk/SM)", "ex2", k_ex2, 8.0*ITERS, 0.0}, {"MIX (candidates/clk/SM)", "mix", k_mix, 2.0*ITERS, 0.0}};
+  printf("{\"sms\": %d", sms);
+  for (auto &t : tests) {
+    double best_clk = 0, best_rate = 0; int best_res = 0;
+    for (int resident : {4, 8}) {   // 256-thread blocks per SM, all co-resident
+      const int blocks = sms * resident, threads = 256;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(cyc, 0, 8); cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+        cudaEventRecord(a); t.k<<<blocks, threads>>>(out, 0.999f, 1e-4f, cyc); cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b); long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        const double per_clk = t.ops * threads * resident / (double)c;      // per SM per SM clock
+        const double per_s = t.ops * (double)threads * blocks / (ms * 1e-3);  // chip, wall clock
+        if (rep == 2) fprintf(stderr, "%-28s blocks/SM=%d  %8.2f per clk per SM  %.3e per s  (%.3f ms, %lld cyc, %.0f MHz)\n",
+                              t.name, resident, per_clk, per_s, ms, c, c / (ms * 1e3));
+        if (rep == 2 && per_s > best_rate) { best_rate = per_s; best_clk = per_clk; best_res = resident; }
+      }
     }
+    printf(", \"%s_per_clk_per_sm\": %.2f, \"%s_per_s\": %.4e", t.key, best_clk, t.key, best_rate);
+    if (t.flop_per_op > 0) printf(", \"%s_tflops\": %.2f", t.key, best_rate * t.flop_per_op / 1e12);
+    (void)best_res;
   }
+  printf("}\n");
   return 0;
 }

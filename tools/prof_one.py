@@ -8,7 +8,7 @@ algo = sys.argv[2] if len(sys.argv) > 2 else "xpencil"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 c = synth.make_config(cfg)
 g = c.grid
-ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=c.n)
+ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=c.n, x_subcells=int(os.environ.get("XSUB", "0")))
 if os.environ.get('TPL') or os.environ.get('TGT') or os.environ.get('THREADS') or os.environ.get('LEN'):
     ctx.set_tuning(xpencil_slots=int(os.environ.get('TPL', '0')), xpencil_targets=int(os.environ.get('TGT', '0')),
                    threads=int(os.environ.get('THREADS', '0')), xpencil_len=int(os.environ.get('LEN', '0')))
