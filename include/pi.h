@@ -78,8 +78,24 @@ typedef enum {
  *                   softening of :582 (reading R19): d~ = sqrt(r_ij^2 + eps^2), u = d~ / r,
  *                   K = 4 E0 (u^12 - u^6); phi_i = sum_j q_j K, F_i = -grad_i (q_i sum_j q_j K);
  *                   the cutoff test uses the unsoftened r_ij.  kparam[0] = r (0 -> r_c),
- *                   kparam[1] = eps (>= 0), kparam[2] = E0 (0 -> 1).                          */
-typedef enum { PI_K_GAUSSIAN = 0, PI_K_INDICATOR = 1, PI_K_CANDIDATE = 2, PI_K_LJ = 3 } pi_kernel;
+ *                   kparam[1] = eps (>= 0), kparam[2] = E0 (0 -> 1).
+ * The two fake kernels of the paper's kernel-cost experiment (Fig. "diffflops", PAPER.md:785-788;
+ * reading R22 of DESIGN.md), with the same cutoff test r_ij < r_c:
+ *   PI_K_LOWFLOP  : "summing the positions" (5 FLOP per interaction): phi_i = sum_j (x_j + y_j +
+ *                   z_j), F_i = sum_j (x_j, y_j, z_j); q is not used.
+ *   PI_K_HIGHFLOP : "the Lennard-Jones kernel with 150 added FLOP" (168 FLOP): PI_K_LJ, whose
+ *                   potential term u = (d~/r)^12 - (d~/r)^6 goes through 75 FMAs t <- t a + b,
+ *                   a = 1 - 2^-7, b = 2^-10 (the affine map A u + B, A = a^75,
+ *                   B = b (1 - A) / (1 - a)) before phi_i = sum_j q_j 4 E0 t; F_i as PI_K_LJ;
+ *                   kparam as PI_K_LJ.                                                       */
+typedef enum {
+  PI_K_GAUSSIAN = 0,
+  PI_K_INDICATOR = 1,
+  PI_K_CANDIDATE = 2,
+  PI_K_LJ = 3,
+  PI_K_LOWFLOP = 4,
+  PI_K_HIGHFLOP = 5
+} pi_kernel;
 
 /* Interaction strategy (a6).
  *   PI_A_GLOBAL  : Par-Part-NoLoop (Alg. 1, §4.1): one thread per target,

@@ -14,6 +14,11 @@
  *            c_ij = (q_j K, q_i q_j K (x_i - x_j)/sigma^2, ...)
  *          1 INDICATOR c_ij = (q_j, 0, 0, 0) inside the cutoff
  *          2 CANDIDATE c_ij = (q_j, 0, 0, 0) for every candidate pair
+ *          3 Lennard-Jones, Eq. (1) with softening (reading R19)
+ *          4 LOWFLOP  c_ij = (x_j + y_j + z_j, x_j, y_j, z_j) inside the cutoff ("summing the
+ *                     positions", reading R22)
+ *          5 HIGHFLOP Lennard-Jones whose potential term u goes through 75 steps t <- t a + b,
+ *                     a = 1 - 2^-7, b = 2^-10, before q_j 4 E0 t ("150 added FLOP")
  * Outputs per requested target t: out[4] (phi, fx, fy, fz), S[4] = sum |c_ij| over
  * included pairs (Lennard-Jones: per Eq. (1) term, reading R20), A[4] = sum |c_ij| over ambiguous pairs (|r^2 - rc^2| <= band rc^2),
  * C = #candidates, P = #pairs inside the cutoff.  All accumulation in double.
@@ -118,12 +123,28 @@ int oracle_interact(int64_t n, const float *x, const float *y, const float *z, c
               cij[1] = qi * w * ddx / s2;
               cij[2] = qi * w * ddy / s2;
               cij[3] = qi * w * ddz / s2;
-            } else if (kernel == 3) {
+            } else if (kernel == 4) {
+              double px = (double)x[j], py = (double)y[j], pz = (double)z[j];
+              cij[0] = px + py + pz;
+              cij[1] = px; cij[2] = py; cij[3] = pz;
+              mag[0] = fabs(px) + fabs(py) + fabs(pz);
+              mag[1] = fabs(px); mag[2] = fabs(py); mag[3] = fabs(pz);
+            } else if (kernel == 3 || kernel == 5) {
               /* d~^2 = d^2 + eps^2, s = (d~ / r)^2: K = 4 E0 (s^6 - s^3),
                  force on i = -q_i q_j dK/dd~ (x_i - x_j) / d~ = q_i q_j G (x_i - x_j) */
               double s = (r2 + ljeps * ljeps) / (ljr * ljr);
               double s3 = s * s * s;
               double K = 4.0 * lje0 * (s3 * s3 - s3);
+              double chainA = 1.0, chainB = 0.0;  /* kernel 5: the chain's |terms| (A, B) */
+              if (kernel == 5) {
+                double t = s3 * s3 - s3;
+                for (int st = 0; st < 75; ++st) {
+                  t = t * (1.0 - 0x1p-7) + 0x1p-10;
+                  chainA *= (1.0 - 0x1p-7);
+                  chainB = chainB * (1.0 - 0x1p-7) + 0x1p-10;
+                }
+                K = 4.0 * lje0 * t;
+              }
               double G = -(4.0 * lje0 / (ljr * ljr)) * (12.0 * s3 * s * s - 6.0 * s * s);
               double w = (double)q[j];
               cij[0] = w * K;
@@ -132,7 +153,7 @@ int oracle_interact(int64_t n, const float *x, const float *y, const float *z, c
               cij[3] = qi * w * G * ddz;
               /* |c_ij| per Eq. (1) term (reading R20): repulsive and attractive
                  parts counted separately, so the tolerance does not vanish where they cancel */
-              double Km = 4.0 * lje0 * (s3 * s3 + s3);
+              double Km = 4.0 * lje0 * (chainA * (s3 * s3 + s3) + chainB);
               double Gm = (4.0 * lje0 / (ljr * ljr)) * (12.0 * s3 * s * s + 6.0 * s * s);
               mag[0] = fabs(w) * Km;
               mag[1] = fabs(qi * w) * Gm * fabs(ddx);
@@ -142,7 +163,7 @@ int oracle_interact(int64_t n, const float *x, const float *y, const float *z, c
               cij[0] = (double)q[j];
               cij[1] = cij[2] = cij[3] = 0.0;
             }
-            if (kernel != 3)
+            if (kernel != 3 && kernel != 4 && kernel != 5)
               for (int m = 0; m < 4; ++m) mag[m] = fabs(cij[m]);
             if (kernel == 2) { inside = 1; ambiguous = 0; }
             if (inside) {

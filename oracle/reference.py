@@ -24,6 +24,26 @@ KERNEL_GAUSSIAN = 0
 KERNEL_INDICATOR = 1
 KERNEL_CANDIDATE = 2
 KERNEL_LJ = 3
+KERNEL_LOWFLOP = 4
+KERNEL_HIGHFLOP = 5
+
+# The kernel-cost sweep's fake kernels (Fig. "diffflops" caption; reading R22):
+#   LOWFLOP  "a fake kernel that costs 5 FLOP per interaction (by summing the positions)":
+#            c_ij = (x_j + y_j + z_j, x_j, y_j, z_j) for r_ij < r_c;
+#   HIGHFLOP "the Lennard-Jones kernel with 150 added FLOP": the LJ potential term
+#            u = (d~/r)^12 - (d~/r)^6 is run through HF_STEPS fused multiply-adds t <- t a + b
+#            (2 FLOP each) before c_ij[0] = q_j 4 E0 t; the force is the LJ force.
+HF_STEPS = 75
+HF_A = 1.0 - 2.0 ** -7
+HF_B = 2.0 ** -10
+
+
+def highflop_chain(u):
+    """The 150 added FLOP, step by step (reading R22)."""
+    t = np.asarray(u, np.float64)
+    for _ in range(HF_STEPS):
+        t = t * HF_A + HF_B
+    return t
 
 
 def lj_params(grid):
@@ -217,6 +237,26 @@ def brute_force(x, y, z, q, grid, kernel=KERNEL_GAUSSIAN, band=None, chunk=512):
             mf = np.abs(Q[s:e, None] * Q[None, :] * Gm)[:, :, None] * np.abs(d)
             mags = np.concatenate([m0[:, :, None], mf], axis=2)
             incl = inside
+        elif kernel == KERNEL_HIGHFLOP:
+            r_, eps_, e0_ = lj_params(grid)
+            K, G = lj_terms(r2, r_, eps_, e0_)
+            u = K / (4.0 * e0_)                                 # (d~/r)^12 - (d~/r)^6
+            c0 = Q[None, :] * 4.0 * e0_ * highflop_chain(u)
+            cf = (Q[s:e, None] * Q[None, :] * G)[:, :, None] * d
+            comps = np.concatenate([c0[:, :, None], cf], axis=2)
+            Km, Gm = lj_term_magnitudes(r2, r_, eps_, e0_)
+            # |terms| of the chain: A |u|_terms + sum_k b a^k = A |u|_terms + B (A = a^75)
+            A_ = HF_A ** HF_STEPS
+            m0 = np.abs(Q[None, :]) * 4.0 * e0_ * (A_ * Km / (4.0 * e0_) + HF_B * (1.0 - A_) / (1.0 - HF_A))
+            mf = np.abs(Q[s:e, None] * Q[None, :] * Gm)[:, :, None] * np.abs(d)
+            mags = np.concatenate([m0[:, :, None], mf], axis=2)
+            incl = inside
+        elif kernel == KERNEL_LOWFLOP:
+            comps = np.zeros(r2.shape + (4,))
+            Xj = X[None, :, :] * np.ones((e - s, 1, 1))
+            comps[:, :, 0] = Xj.sum(axis=2)
+            comps[:, :, 1:] = Xj
+            incl = inside
         elif kernel == KERNEL_INDICATOR:
             comps = np.zeros(r2.shape + (4,))
             comps[:, :, 0] = Q[None, :]
@@ -228,8 +268,11 @@ def brute_force(x, y, z, q, grid, kernel=KERNEL_GAUSSIAN, band=None, chunk=512):
             amb = np.zeros_like(amb)
         else:
             raise ValueError(kernel)
-        if kernel != KERNEL_LJ:
+        if kernel not in (KERNEL_LJ, KERNEL_HIGHFLOP):
             mags = np.abs(comps)
+        if kernel == KERNEL_LOWFLOP:  # per component term: |x_j| + |y_j| + |z_j| for phi
+            mags = np.abs(comps)
+            mags[:, :, 0] = np.abs(Xj).sum(axis=2)
         out[s:e] = np.einsum("ij,ijk->ik", incl.astype(np.float64), comps)
         S[s:e] = np.einsum("ij,ijk->ik", incl.astype(np.float64), mags)
         A[s:e] = np.einsum("ij,ijk->ik", amb.astype(np.float64), mags)

@@ -37,7 +37,7 @@ def _config(dims, cell_width, r_c=None, origin=(0.0, 0.0, 0.0), kernel="gaussian
     cfg.cell_width = float(cell_width)
     cfg.r_c = float(cell_width if r_c is None else r_c)
     cfg.kernel = L.KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
-    if cfg.kernel == L.KERNELS["lj"]:  # Lennard-Jones r, eps, E0 (0 -> r_c, 0, 1)
+    if cfg.kernel in (L.KERNELS["lj"], L.KERNELS["highflop"]):  # Lennard-Jones r, eps, E0 (0 -> r_c, 0, 1)
         for k in range(3):
             cfg.kparam[k] = float(lj[k])
     else:

@@ -208,8 +208,8 @@ static bool config_ok(const pi_config *cfg, char *why, size_t n) {
   if (!(cfg->cell_width > 0.f)) { snprintf(why, n, "cell_width must be > 0"); return false; }
   if (!(cfg->r_c > 0.f)) { snprintf(why, n, "r_c must be > 0"); return false; }
   if (cfg->r_c > cfg->cell_width) { snprintf(why, n, "cell_width must be >= r_c (PAPER.md:93)"); return false; }
-  if (cfg->kernel < 0 || cfg->kernel > 3) { snprintf(why, n, "unknown kernel"); return false; }
-  if (cfg->kernel == PI_K_LJ && (cfg->kparam[0] < 0.f || cfg->kparam[1] < 0.f)) {
+  if (cfg->kernel < 0 || cfg->kernel > 5) { snprintf(why, n, "unknown kernel"); return false; }
+  if ((cfg->kernel == PI_K_LJ || cfg->kernel == PI_K_HIGHFLOP) && (cfg->kparam[0] < 0.f || cfg->kparam[1] < 0.f)) {
     snprintf(why, n, "Lennard-Jones r and eps must be >= 0");
     return false;
   }
@@ -327,7 +327,7 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
   k.s_inv = (float)(1.0 / std::sqrt((double)k.c2));
   k.phi_scale = 1.0f;
   k.f_ts = k.inv_s2;
-  if (cfg->kernel == PI_K_LJ) {  // Eq. (1), reading R19
+  if (cfg->kernel == PI_K_LJ || cfg->kernel == PI_K_HIGHFLOP) {  // Eq. (1), reading R19
     const double r = cfg->kparam[0] > 0.f ? cfg->kparam[0] : cfg->r_c;
     const double eps = cfg->kparam[1];
     const double e0 = cfg->kparam[2] > 0.f ? cfg->kparam[2] : 1.0;

@@ -138,13 +138,16 @@ __device__ void cs_targets(const CsParams &p, int t0, int tbase, int nt, int P, 
 #pragma unroll
   for (int k = 0; k < TPT; ++k) {
     if (!ok[k] || gi > 0) continue;
-    const float phi = lo(acc[k][0]) + hi(acc[k][0]) - self_term<KERNEL>(me[k].w, p.kp);
-    const float sx_ = lo(acc[k][1]) + hi(acc[k][1]), sy_ = lo(acc[k][2]) + hi(acc[k][2]);
-    const float sz_ = lo(acc[k][3]) + hi(acc[k][3]);
+    const float4 st = self_terms<KERNEL>(me[k], p.kp);  // identity exclusion (Alg. 1 :127)
+    const float phi = lo(acc[k][0]) + hi(acc[k][0]) - st.x;
+    const float sx_ = lo(acc[k][1]) + hi(acc[k][1]) - st.y, sy_ = lo(acc[k][2]) + hi(acc[k][2]) - st.z;
+    const float sz_ = lo(acc[k][3]) + hi(acc[k][3]) - st.w;
     const int t = t0 + tbase + ti + k * NT;
-    if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+    if (kern_wforce(KERNEL)) {
       const float sc = -me[k].w * p.kp.f_ts;  // the walk summed wf (x_s - x_t)
       write_output<UPD>(p.out, p.g, t, me[k], phi * p.kp.phi_scale, sc * sx_, sc * sy_, sc * sz_);
+    } else if (KERNEL == PI_K_LOWFLOP) {
+      write_output<UPD>(p.out, p.g, t, me[k], phi, sx_, sy_, sz_);
     } else {
       write_output<UPD>(p.out, p.g, t, me[k], phi, 0.f, 0.f, 0.f);
     }

@@ -114,9 +114,35 @@ __device__ __forceinline__ SrcPair load_pair(const float4 *__restrict__ A, const
   return r;
 }
 
+// The kernel-cost sweep's fake kernels (Fig. "diffflops"; reading R22):
+//   PI_K_LOWFLOP  "summing the positions": c_ij = (x_j + y_j + z_j, x_j, y_j, z_j) inside r_c;
+//   PI_K_HIGHFLOP "the Lennard-Jones kernel with 150 added FLOP": Eq. (1), its potential term
+//                 u = s^6 - s^3 run through 75 FMAs t <- t a + b (150 FLOP) before the value
+//                 q_j 4 E0 t is summed (the force is the LJ force).  a = 1 - 2^-7, b = 2^-10: the
+//                 chain is the affine map A u + B, A = a^75, B = b (1 - A) / (1 - a).
+__host__ __device__ constexpr bool kern_lj(int k) { return k == PI_K_LJ || k == PI_K_HIGHFLOP; }
+__host__ __device__ constexpr bool kern_wforce(int k) { return k == PI_K_GAUSSIAN || kern_lj(k); }
+constexpr int HF_STEPS = 75;
+constexpr float HF_A = 0.9921875f;  // 1 - 2^-7
+constexpr float HF_B = 0x1p-10f;
+__device__ __forceinline__ p2 hf_chain(p2 t) {
+#pragma unroll 15
+  for (int k = 0; k < HF_STEPS; ++k) t = fma2(t, pk(HF_A), pk(HF_B));
+  return t;
+}
+__device__ __forceinline__ float hf_chain1(float t) {  // the same rounded operations, one value
+#pragma unroll 15
+  for (int k = 0; k < HF_STEPS; ++k) t = fmaf(t, HF_A, HF_B);
+  return t;
+}
+// LOWFLOP: the sum of a source's position components, in the order every strategy uses
+__device__ __forceinline__ float lf_sum(float x, float y, float z) { return __fadd_rn(__fadd_rn(x, y), z); }
+__device__ __forceinline__ p2 lf_sum2(p2 x, p2 y, p2 z) { return add2(add2(x, y), z); }
+
 // Lennard-Jones core (Eq. (1), reading R19) on f32x2 values: s = (d~/r)^2 = r2 / r^2 + eps^2 / r^2;
 // returns the potential and force weights of the pair halves with q masked to the cutoff
 // (qm = r2 < r_c^2 ? q : 0):  w = qm (s^6 - s^3),  wf = qm (12 s^5 - 6 s^2).
+template <int KERNEL = PI_K_LJ>
 __device__ __forceinline__ void lj_core(p2 r2, p2 q, const float thr, const KParams &kp, p2 &w, p2 &wf) {
   // clamp to r_c^2 before the powers: an inert padding partner (x = 1e30) would give s = inf,
   // inf - inf = NaN and NaN * 0 = NaN; masked halves only need finite values
@@ -126,7 +152,8 @@ __device__ __forceinline__ void lj_core(p2 r2, p2 q, const float thr, const KPar
   const p2 s3 = mul2(s2, s);
   const p2 s6 = mul2(s3, s3);
   const p2 s5 = mul2(s3, s2);
-  const p2 pot = add2(s6, pk(-lo(s3), -hi(s3)));
+  p2 pot = add2(s6, pk(-lo(s3), -hi(s3)));
+  if (KERNEL == PI_K_HIGHFLOP) pot = hf_chain(pot);
   const p2 fk = fma2(s5, pk(12.f), mul2(s2, pk(-6.f)));
   const p2 qm = pk((lo(r2) < thr) ? lo(q) : 0.f, (hi(r2) < thr) ? hi(q) : 0.f);
   w = mul2(pot, qm);
@@ -159,9 +186,16 @@ __device__ __forceinline__ void src_eval(const SrcPair &s, float xt, float yt, f
     fx = fma2(w, dx, fx);
     fy = fma2(w, dy, fy);
     fz = fma2(w, dz, fz);
-  } else if (KERNEL == PI_K_LJ) {
+  } else if (KERNEL == PI_K_LOWFLOP) {  // selects, not products: an inert partner is at 1e30
+    const bool i0 = lo(r2) < thr, i1 = hi(r2) < thr;
+    const p2 sm = lf_sum2(s.x, s.y, s.z);
+    phi = add2(phi, pk(i0 ? lo(sm) : 0.f, i1 ? hi(sm) : 0.f));
+    fx = add2(fx, pk(i0 ? lo(s.x) : 0.f, i1 ? hi(s.x) : 0.f));
+    fy = add2(fy, pk(i0 ? lo(s.y) : 0.f, i1 ? hi(s.y) : 0.f));
+    fz = add2(fz, pk(i0 ? lo(s.z) : 0.f, i1 ? hi(s.z) : 0.f));
+  } else if (kern_lj(KERNEL)) {
     p2 w, wf;
-    lj_core(r2, s.q, thr, *kp, w, wf);
+    lj_core<KERNEL>(r2, s.q, thr, *kp, w, wf);
     phi = add2(phi, w);
     fx = fma2(wf, dx, fx);
     fy = fma2(wf, dy, fy);
@@ -178,20 +212,29 @@ __device__ __forceinline__ void src_eval(const SrcPair &s, float xt, float yt, f
 // operations as lj_core at r2 = 0 (fma(0, ., e2) = e2), so the subtraction is exact.
 template <int KERNEL>
 __device__ __forceinline__ float self_term(float q, const KParams &kp) {
-  if (KERNEL != PI_K_LJ) return q;
+  if (!kern_lj(KERNEL)) return q;
   const float s = kp.lj_e2;
   const float s2 = __fmul_rn(s, s), s3 = __fmul_rn(s2, s), s6 = __fmul_rn(s3, s3);
-  return __fmul_rn(__fsub_rn(s6, s3), q);
+  float pot = __fsub_rn(s6, s3);
+  if (KERNEL == PI_K_HIGHFLOP) pot = hf_chain1(pot);
+  return __fmul_rn(pot, q);
+}
+// The self pair's full term (phi, F accumulators) for target me: LOWFLOP sums the positions,
+// so its self pair adds (x + y + z, x, y, z); every other kernel adds (self_term, 0, 0, 0).
+template <int KERNEL>
+__device__ __forceinline__ float4 self_terms(const float4 &me, const KParams &kp) {
+  if (KERNEL == PI_K_LOWFLOP) return make_float4(lf_sum(me.x, me.y, me.z), me.x, me.y, me.z);
+  return make_float4(self_term<KERNEL>(me.w, kp), 0.f, 0.f, 0.f);
 }
 
 // Scalar contribution of a source of value qs at squared distance r2 (inside the cutoff):
 // w (phi, before phi_scale) and wf (force weight: F += wf (x_t - x_s), before q_t f_ts).
 template <int KERNEL>
 __device__ __forceinline__ void scalar_term(const KParams &kp, float r2, float qs, float &w, float &wf) {
-  if (KERNEL == PI_K_LJ) {
+  if (kern_lj(KERNEL)) {
     const float s = fmaf(r2, kp.lj_inv_r2, kp.lj_e2);
     const float s2 = s * s, s3 = s2 * s, s6 = s3 * s3, s5 = s3 * s2;
-    w = (s6 - s3) * qs;
+    w = (KERNEL == PI_K_HIGHFLOP ? hf_chain1(s6 - s3) : (s6 - s3)) * qs;
     wf = fmaf(s5, 12.f, s2 * -6.f) * qs;
   } else {
     w = qs * ex2_approx(-kp.c2 * r2);

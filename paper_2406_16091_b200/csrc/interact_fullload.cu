@@ -75,13 +75,20 @@ __device__ __forceinline__ void tp_eval(const TgtPair &t, const float4 a, const 
     fx = fma2(w, dx, fx);
     fy = fma2(w, dy, fy);
     fz = fma2(w, dz, fz);
-  } else if (KERNEL == PI_K_LJ) {
+  } else if (kern_lj(KERNEL)) {
     p2 w, wf;
-    lj_core(r2, pk(a.w), thr, kp, w, wf);
+    lj_core<KERNEL>(r2, pk(a.w), thr, kp, w, wf);
     phi = add2(phi, w);
     fx = fma2(wf, dx, fx);
     fy = fma2(wf, dy, fy);
     fz = fma2(wf, dz, fz);
+  } else if (KERNEL == PI_K_LOWFLOP) {  // selects (an inert partner is at 1e30)
+    const bool i0 = lo(r2) < thr, i1 = hi(r2) < thr;
+    const float sm = lf_sum(a.x, a.y, a.z);
+    phi = add2(phi, pk(i0 ? sm : 0.f, i1 ? sm : 0.f));
+    fx = add2(fx, pk(i0 ? a.x : 0.f, i1 ? a.x : 0.f));
+    fy = add2(fy, pk(i0 ? a.y : 0.f, i1 ? a.y : 0.f));
+    fz = add2(fz, pk(i0 ? a.z : 0.f, i1 ? a.z : 0.f));
   } else {
     phi = add2(phi, pk((lo(r2) < thr) ? a.w : 0.f, (hi(r2) < thr) ? a.w : 0.f));
   }
@@ -92,7 +99,8 @@ template <int KERNEL>
 __device__ __forceinline__ float tp_self(const TgtPair &t, int h, const float4 a, const float thr, const float mc2,
                                          const KParams &kp) {
   if (KERNEL == PI_K_CANDIDATE) return a.w;
-  if (KERNEL == PI_K_LJ) {  // the same lj_core operations as tp_eval, this half
+  if (KERNEL == PI_K_LOWFLOP) return lf_sum(a.x, a.y, a.z);
+  if (kern_lj(KERNEL)) {  // the same lj_core operations as tp_eval, this half
     const p2 dx = add2(t.x, pk(-a.x));
     const p2 dy = add2(t.y, pk(-a.y));
     const p2 dz = add2(t.z, pk(-a.z));
@@ -100,7 +108,7 @@ __device__ __forceinline__ float tp_self(const TgtPair &t, int h, const float4 a
     r2 = fma2(dy, dy, r2);
     r2 = fma2(dz, dz, r2);
     p2 w, wf;
-    lj_core(r2, pk(a.w), thr, kp, w, wf);
+    lj_core<KERNEL>(r2, pk(a.w), thr, kp, w, wf);
     return h ? hi(w) : lo(w);
   }
   const p2 dx = add2(t.x, pk(-a.x));
@@ -253,20 +261,29 @@ __global__ void __launch_bounds__(NT) k_interact_fullload(FlParams p) {
       // identity exclusion (Alg. 1 :127)
       phi = pk(lo(phi) - tp_self<KERNEL>(tp, 0, a0, thr, mc2, p.kp), hi(phi));
       if (t1 != t0) phi = pk(lo(phi), hi(phi) - tp_self<KERNEL>(tp, 1, a1, thr, mc2, p.kp));
+      if (KERNEL == PI_K_LOWFLOP) {  // the self pair also added the target's own position
+        fx = pk(lo(fx) - a0.x, t1 != t0 ? hi(fx) - a1.x : hi(fx));
+        fy = pk(lo(fy) - a0.y, t1 != t0 ? hi(fy) - a1.y : hi(fy));
+        fz = pk(lo(fz) - a0.z, t1 != t0 ? hi(fz) - a1.z : hi(fz));
+      }
       cand += (unsigned long long)(t1 - t0 + 1) * (unsigned long long)(ncand - 1);
       const int gs0 = O[rh * BX3 + cx + 1] + 2 * i;
       const float4 me0 = p.out.upd ? __ldg(p.rec + gs0) : a0;
-      if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+      if (kern_wforce(KERNEL)) {
         const float c0 = a0.w * p.kp.f_ts;  // summed wf (x_t - x_s)
         write_output(p.out, g, gs0, me0, lo(phi) * p.kp.phi_scale, c0 * lo(fx), c0 * lo(fy), c0 * lo(fz));
+      } else if (KERNEL == PI_K_LOWFLOP) {
+        write_output(p.out, g, gs0, me0, lo(phi), lo(fx), lo(fy), lo(fz));
       } else {
         write_output(p.out, g, gs0, me0, lo(phi), 0.f, 0.f, 0.f);
       }
       if (t1 != t0) {
         const float4 me1 = p.out.upd ? __ldg(p.rec + gs0 + 1) : a1;
-        if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+        if (kern_wforce(KERNEL)) {
           const float c1 = a1.w * p.kp.f_ts;
           write_output(p.out, g, gs0 + 1, me1, hi(phi) * p.kp.phi_scale, c1 * hi(fx), c1 * hi(fy), c1 * hi(fz));
+        } else if (KERNEL == PI_K_LOWFLOP) {
+          write_output(p.out, g, gs0 + 1, me1, hi(phi), hi(fx), hi(fy), hi(fz));
         } else {
           write_output(p.out, g, gs0 + 1, me1, hi(phi), 0.f, 0.f, 0.f);
         }
@@ -297,6 +314,8 @@ cudaError_t launch_nt(const FlParams &p, cudaStream_t s) {
     case PI_K_GAUSSIAN: return launch_k<PI_K_GAUSSIAN, NT>(p, s);
     case PI_K_INDICATOR: return launch_k<PI_K_INDICATOR, NT>(p, s);
     case PI_K_LJ: return launch_k<PI_K_LJ, NT>(p, s);
+    case PI_K_LOWFLOP: return launch_k<PI_K_LOWFLOP, NT>(p, s);
+    case PI_K_HIGHFLOP: return launch_k<PI_K_HIGHFLOP, NT>(p, s);
     default: return launch_k<PI_K_CANDIDATE, NT>(p, s);
   }
 }
@@ -380,6 +399,8 @@ cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const Inte
     case PI_K_GAUSSIAN: return upd ? go(k_cellsm_list<PI_K_GAUSSIAN, true>) : go(k_cellsm_list<PI_K_GAUSSIAN, false>);
     case PI_K_INDICATOR: return upd ? go(k_cellsm_list<PI_K_INDICATOR, true>) : go(k_cellsm_list<PI_K_INDICATOR, false>);
     case PI_K_LJ: return upd ? go(k_cellsm_list<PI_K_LJ, true>) : go(k_cellsm_list<PI_K_LJ, false>);
+    case PI_K_LOWFLOP: return upd ? go(k_cellsm_list<PI_K_LOWFLOP, true>) : go(k_cellsm_list<PI_K_LOWFLOP, false>);
+    case PI_K_HIGHFLOP: return upd ? go(k_cellsm_list<PI_K_HIGHFLOP, true>) : go(k_cellsm_list<PI_K_HIGHFLOP, false>);
     default: return upd ? go(k_cellsm_list<PI_K_CANDIDATE, true>) : go(k_cellsm_list<PI_K_CANDIDATE, false>);
   }
 }

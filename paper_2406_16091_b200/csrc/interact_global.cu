@@ -58,6 +58,11 @@ __global__ void __launch_bounds__(PPNL_THREADS) k_interact_global(long long n, c
           } else if (r2 < kp.rc2) {
             if (KERNEL == PI_K_INDICATOR) {
               phi += o.w;
+            } else if (KERNEL == PI_K_LOWFLOP) {
+              phi += lf_sum(o.x, o.y, o.z);
+              fx += o.x;
+              fy += o.y;
+              fz += o.z;
             } else {
               float w, wf;
               scalar_term<KERNEL>(kp, r2, o.w, w, wf);
@@ -71,10 +76,11 @@ __global__ void __launch_bounds__(PPNL_THREADS) k_interact_global(long long n, c
       }
     }
     cand -= 1;  // self
-    if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+    if (kern_wforce(KERNEL)) {
       const float s = me.w * kp.f_ts;  // summed wf (x_t - x_s)
       phi *= kp.phi_scale;
       fx *= s; fy *= s; fz *= s;
+    } else if (KERNEL == PI_K_LOWFLOP) {
     } else {
       fx = fy = fz = 0.f;
     }
@@ -101,6 +107,14 @@ cudaError_t launch_interact_global(const Geom &g, const KParams &k, const Intera
       break;
     case PI_K_LJ:
       k_interact_global<PI_K_LJ><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl, a.n_dev);
+      break;
+    case PI_K_LOWFLOP:
+      k_interact_global<PI_K_LOWFLOP><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl,
+                                                                       a.n_dev);
+      break;
+    case PI_K_HIGHFLOP:
+      k_interact_global<PI_K_HIGHFLOP><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl,
+                                                                        a.n_dev);
       break;
     default:
       k_interact_global<PI_K_CANDIDATE><<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.offsets, g, k, a.out, a.ctl,

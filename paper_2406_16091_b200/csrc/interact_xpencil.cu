@@ -241,10 +241,11 @@ __device__ __forceinline__ float4 walk9(const Slot &sl, int LF, int sx, int ja, 
   fx = add2(fx, fxb);
   fy = add2(fy, fyb);
   fz = add2(fz, fzb);
-  // identity exclusion (Alg. 1 :127): remove the exact term the self pair added to phi
-  // (q_t, or the LJ value at d = 0; it added nothing to F)
-  return make_float4(lo(phi) + hi(phi) - self_term<KERNEL>(me.w, kp), lo(fx) + hi(fx), lo(fy) + hi(fy),
-                     lo(fz) + hi(fz));
+  // identity exclusion (Alg. 1 :127): remove the exact term the self pair added (q_t, or the LJ
+  // value at d = 0, to phi only; LOWFLOP: the target's own position sums)
+  const float4 st = self_terms<KERNEL>(me, kp);
+  return make_float4(lo(phi) + hi(phi) - st.x, lo(fx) + hi(fx) - st.y, lo(fy) + hi(fy) - st.z,
+                     lo(fz) + hi(fz) - st.w);
 }
 
 // Two targets per lane (the register blocking of the paper's X-pencil-reg idea, PAPER.md
@@ -284,10 +285,11 @@ __device__ __forceinline__ void walk9x2(const Slot &sl, int LF, int sx, int ja, 
     }
   }
   // identity exclusion (Alg. 1 :127): each target's own self pair was evaluated in the window
-  r0 = make_float4(lo(ph0) + hi(ph0) - self_term<KERNEL>(me0.w, kp), lo(fx0) + hi(fx0), lo(fy0) + hi(fy0),
-                   lo(fz0) + hi(fz0));
-  r1 = make_float4(lo(ph1) + hi(ph1) - self_term<KERNEL>(me1.w, kp), lo(fx1) + hi(fx1), lo(fy1) + hi(fy1),
-                   lo(fz1) + hi(fz1));
+  const float4 s0 = self_terms<KERNEL>(me0, kp), s1 = self_terms<KERNEL>(me1, kp);
+  r0 = make_float4(lo(ph0) + hi(ph0) - s0.x, lo(fx0) + hi(fx0) - s0.y, lo(fy0) + hi(fy0) - s0.z,
+                   lo(fz0) + hi(fz0) - s0.w);
+  r1 = make_float4(lo(ph1) + hi(ph1) - s1.x, lo(fx1) + hi(fx1) - s1.y, lo(fy1) + hi(fy1) - s1.z,
+                   lo(fz1) + hi(fz1) - s1.w);
 }
 
 // UPD: pi_step (update + carried counts in the epilogue); TPL: targets per lane (1: walk9, 2: walk9x2)
@@ -458,9 +460,11 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       auto finish = [&](int gs, int j, int sub, const float4 &me, const float4 &r) {
         int fold = -1;
         if (UPD && p.out.pcounts) fold = ((x0 - 1 + j) * sx + sub) + ((g.nx * (cy + g.ny * cz)) << g.sxs);
-        if (KERNEL == PI_K_GAUSSIAN || KERNEL == PI_K_LJ) {
+        if (kern_wforce(KERNEL)) {
           const float sc = -me.w * p.kp.f_ts;  // the walk summed wf (x_s - x_t)
           write_output<UPD>(p.out, g, gs, me, r.x * p.kp.phi_scale, sc * r.y, sc * r.z, sc * r.w, fold);
+        } else if (KERNEL == PI_K_LOWFLOP) {
+          write_output<UPD>(p.out, g, gs, me, r.x, r.y, r.z, r.w, fold);
         } else {
           write_output<UPD>(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f, fold);
         }
@@ -564,6 +568,10 @@ cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
     case PI_K_LJ:
       if (two) return upd ? go(k_interact_xpencil<PI_K_LJ, NC, true, 2>) : go(k_interact_xpencil<PI_K_LJ, NC, false, 2>);
       return upd ? go(k_interact_xpencil<PI_K_LJ, NC, true, 1>) : go(k_interact_xpencil<PI_K_LJ, NC, false, 1>);
+    case PI_K_LOWFLOP:
+      return upd ? go(k_interact_xpencil<PI_K_LOWFLOP, NC, true, 1>) : go(k_interact_xpencil<PI_K_LOWFLOP, NC, false, 1>);
+    case PI_K_HIGHFLOP:
+      return upd ? go(k_interact_xpencil<PI_K_HIGHFLOP, NC, true, 1>) : go(k_interact_xpencil<PI_K_HIGHFLOP, NC, false, 1>);
     default:
       return upd ? go(k_interact_xpencil<PI_K_CANDIDATE, NC, true, 1>)
                  : go(k_interact_xpencil<PI_K_CANDIDATE, NC, false, 1>);
@@ -598,6 +606,8 @@ cudaError_t launch_dense_rest(const XpParams &p, cudaStream_t s) {
     case PI_K_GAUSSIAN: return upd ? go(k_cellsm_list<PI_K_GAUSSIAN, true>) : go(k_cellsm_list<PI_K_GAUSSIAN, false>);
     case PI_K_INDICATOR: return upd ? go(k_cellsm_list<PI_K_INDICATOR, true>) : go(k_cellsm_list<PI_K_INDICATOR, false>);
     case PI_K_LJ: return upd ? go(k_cellsm_list<PI_K_LJ, true>) : go(k_cellsm_list<PI_K_LJ, false>);
+    case PI_K_LOWFLOP: return upd ? go(k_cellsm_list<PI_K_LOWFLOP, true>) : go(k_cellsm_list<PI_K_LOWFLOP, false>);
+    case PI_K_HIGHFLOP: return upd ? go(k_cellsm_list<PI_K_HIGHFLOP, true>) : go(k_cellsm_list<PI_K_HIGHFLOP, false>);
     default: return upd ? go(k_cellsm_list<PI_K_CANDIDATE, true>) : go(k_cellsm_list<PI_K_CANDIDATE, false>);
   }
 }

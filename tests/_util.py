@@ -12,7 +12,7 @@ def ctx_for(cloud, kernel="gaussian", capacity=None, **kw):
     from paper_2406_16091_b200 import Context
     g = cloud.grid
     cap = capacity if capacity is not None else max(cloud.n, 1)
-    if kernel == "lj":
+    if kernel in ("lj", "highflop"):
         kw.setdefault("lj", (g.lj_ref, g.lj_soft, g.lj_e0))
     return Context(g.dims, g.w, g.r_c, g.origin, kernel=kernel, sigma=0.0 if g.sigma is None else g.sigma,
                    capacity=cap, device="cuda", **kw)
@@ -36,7 +36,7 @@ def gpu_interact(cloud, algo, kernel="gaussian", tuning=None, ctx=None):
 
 
 KERNEL_ID = {"gaussian": ref.KERNEL_GAUSSIAN, "indicator": ref.KERNEL_INDICATOR, "candidate": ref.KERNEL_CANDIDATE,
-             "lj": ref.KERNEL_LJ}
+             "lj": ref.KERNEL_LJ, "lowflop": ref.KERNEL_LOWFLOP, "highflop": ref.KERNEL_HIGHFLOP}
 
 
 def oracle_interact(cloud, kernel="gaussian", targets=None, band=None):

@@ -18,7 +18,7 @@ ALGOS = ["global", "xpencil", "fullload"]
 
 
 @pytest.mark.parametrize("algo", ALGOS)
-@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate", "lj"])
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate", "lj", "lowflop", "highflop"])
 def test_c0_full(algo, kernel):
     """configs[0]: 4096 uniform particles, 16^3 cells, every particle vs the oracle."""
     c = synth.make_config("c0")
@@ -319,3 +319,19 @@ def test_c4_full_size_sampled():
     sample = np.random.default_rng(7).choice(c.n, 3000, replace=False)
     assert_parity(got[sample], oracle_interact(c, targets=sample), label="c4 xpencil")
     assert ctx.stats()["candidates"] == oracle_candidates(c)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("kernel", ["lowflop", "highflop"])
+@pytest.mark.parametrize("ppc", [2, 20])
+def test_cost_sweep_kernels(algo, kernel, ppc):
+    """The kernel-cost sweep's fake kernels (reading R22) at two densities, and
+    an isolated particle exactly 0 (the self pair removed exactly, positions included)."""
+    c = synth.scaled_uniform(ppc, (12, 10, 9), seed=240616097 + ppc)
+    got, _ = gpu_interact(c, algo, kernel)
+    assert_parity(got, oracle_interact(c, kernel), label=f"{kernel} ppc{ppc} {algo}")
+    grid = synth.Grid(dims=(4, 4, 4), w=0.25)
+    one = synth.Cloud(grid, np.array([0.3], np.float32), np.array([0.6], np.float32), np.array([0.9], np.float32),
+                      np.array([1.5], np.float32))
+    got, _ = gpu_interact(one, algo, kernel)
+    assert np.all(got == 0)

@@ -545,3 +545,49 @@ def test_lj_term_magnitudes_hand_values():
     Km, Gm = ref.lj_term_magnitudes(u2, 1.0, 0.0, 1.0)
     K, G = ref.lj_terms(u2, 1.0, 0.0, 1.0)
     assert abs(G) < 1e-12 and Gm == pytest.approx(4 * 12 * u2 ** 2, rel=1e-12)
+
+
+# ---------------------------------------------------------------- kernel-cost sweep (R22)
+
+def test_lowflop_hand_values():
+    """LOWFLOP ("summing the positions"): two particles within r_c get each other's
+    position and its component sum, a third beyond r_c nothing; dyadic values are exact."""
+    grid = synth.Grid(dims=(4, 4, 4), w=0.25)
+    f = np.float32
+    x, y, z = np.array([0.25, 0.375, 0.875], f), np.array([0.5, 0.5, 0.5], f), np.array([0.125, 0.25, 0.125], f)
+    q = np.ones(3, f)
+    for r in (ref.brute_force(x, y, z, q, grid, kernel=ref.KERNEL_LOWFLOP),
+              celllist.interact(x, y, z, q, grid, kernel=ref.KERNEL_LOWFLOP)):
+        o = r["out"]
+        assert o[0].tolist() == [0.375 + 0.5 + 0.25, 0.375, 0.5, 0.25]
+        assert o[1].tolist() == [0.25 + 0.5 + 0.125, 0.25, 0.5, 0.125]
+        assert o[2].tolist() == [0.0, 0.0, 0.0, 0.0] and r["P"].tolist() == [1, 1, 0]
+
+
+def test_highflop_chain_closed_form():
+    """HIGHFLOP's 75-step chain t <- t a + b (the '150 added FLOP') equals the affine
+    map A u + B with A = a^75, B = b (1 - a^75) / (1 - a) (geometric series), and the oracle's
+    pair value is q_j 4 E0 (A u + B) with u the LJ term of Eq. (1)."""
+    u = np.array([-0.25, 0.0, 0.7, 3.0])
+    A = ref.HF_A ** ref.HF_STEPS
+    B = ref.HF_B * (1 - A) / (1 - ref.HF_A)
+    assert np.allclose(ref.highflop_chain(u), A * u + B, rtol=1e-14, atol=1e-15)
+    grid = synth.Grid(dims=(2, 2, 2), w=1.0, lj_r=1.0, lj_eps=0.0, lj_e0=1.0)
+    f = np.float32
+    x, y, z = np.array([0.25, 0.75], f), np.array([0.5, 0.5], f), np.array([0.5, 0.5], f)
+    q = np.array([1.5, 0.5], f)
+    want0 = 0.5 * 4.0 * (A * (-252.0 / 4096.0 / 4.0) + B)   # u = 1/4096 - 1/64 at d = 1/2 (test_lj_hand_values)
+    for r in (ref.brute_force(x, y, z, q, grid, kernel=ref.KERNEL_HIGHFLOP),
+              celllist.interact(x, y, z, q, grid, kernel=ref.KERNEL_HIGHFLOP)):
+        assert r["out"][0, 0] == pytest.approx(want0, rel=1e-13)
+        assert r["out"][0, 1] == 1.5 * 0.5 * 1.453125 * -0.5  # the LJ force, unchanged
+
+
+@pytest.mark.parametrize("kernel", [ref.KERNEL_LOWFLOP, ref.KERNEL_HIGHFLOP])
+def test_cost_kernels_celllist_equals_brute_force(kernel):
+    c = synth.scaled_uniform(6, (8, 7, 6), seed=31)
+    a = ref.brute_force(c.x, c.y, c.z, c.q, c.grid, kernel=kernel)
+    b = celllist.interact(c.x, c.y, c.z, c.q, c.grid, kernel=kernel)
+    assert np.array_equal(a["P"], b["P"])
+    assert np.allclose(a["out"], b["out"], rtol=1e-12, atol=1e-12)
+    assert np.allclose(a["S"], b["S"], rtol=1e-12, atol=1e-12)

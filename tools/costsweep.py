@@ -1,8 +1,9 @@
-"""Kernel-cost sweep (the paper's Fig. "diffflops" experiment, with this
-library's kernels instead of the paper's unspecified fake kernels): one workload, every
-interaction strategy, kernels from cheap to costly -- CANDIDATE (count every 27-cell
-candidate: no distance), INDICATOR (distance + cutoff test), Gaussian (+ ex2), Lennard-Jones
-(+ 6 powers).  Interaction kernel only, 200 back-to-back calls as PAPER.md:549.
+"""Kernel-cost sweep (the paper's Fig. "diffflops" experiment): one workload,
+every interaction strategy, kernels from cheap to costly -- CANDIDATE (count every 27-cell
+candidate: no distance), INDICATOR (distance + cutoff test), the paper's 5-FLOP fake kernel
+LOWFLOP ("summing the positions"), Gaussian (+ ex2), Lennard-Jones (Eq. (1), the paper's 18-21
+FLOP kernel) and the paper's 168-FLOP fake kernel HIGHFLOP (LJ + 150 FLOP; reading R22).
+Interaction kernel only, 200 back-to-back calls as PAPER.md:549.
 Context for DESIGN.md; bench.py is the contract.
 
 usage: python tools/costsweep.py [--config c1] [--calls 200]"""
@@ -26,9 +27,9 @@ c = synth.make_config(a.config)
 g = c.grid
 t = [torch.from_numpy(v).cuda() for v in (c.x, c.y, c.z, c.q)]
 rows = []
-for kernel in ("candidate", "indicator", "gaussian", "lj"):
+for kernel in ("candidate", "indicator", "lowflop", "gaussian", "lj", "highflop"):
     ctx = Context(g.dims, g.w, g.r_c, g.origin, kernel=kernel, capacity=c.n,
-                  lj=(g.lj_ref, g.lj_soft, g.lj_e0) if kernel == "lj" else (0, 0, 0))
+                  lj=(g.lj_ref, g.lj_soft, g.lj_e0) if kernel in ("lj", "highflop") else (0, 0, 0))
     ctx.bin(*t)
     line = f"{kernel:10s}"
     for algo in a.algos.split(","):
@@ -45,6 +46,7 @@ for kernel in ("candidate", "indicator", "gaussian", "lj"):
         rows.append(dict(config=a.config, kernel=kernel, algo=algo, seconds=sec, candidates=C, rate=C / sec))
         line += f"  {algo} {sec * 1e6:8.1f} us ({C / sec:.3e} cand/s)"
     print(line, flush=True)
+    ctx.close()
     del ctx
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(rows, open(f"gpurun_out/costsweep_{a.config}.json", "w"), indent=1)
