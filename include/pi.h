@@ -150,10 +150,11 @@ typedef struct {
   int64_t migrants_in;       /* particles received by the last migration (nranks > 1)       */
   int64_t migrants_out;      /* particles sent by the last migration (nranks > 1)           */
   int64_t steps;             /* pi_step calls so far                                          */
+  int64_t exchange_bytes;    /* a8: payload bytes this rank sent to its neighbours so far      */
   double phase_ms[4];        /* device time of the last bin (a1-a4), interaction (a5-a7),
                                 exchange (a8) and host-path copies, from CUDA events recorded
                                 on the context stream around each phase                      */
-  int64_t reserved[4];
+  int64_t reserved[3];
 } pi_stats;
 
 /* Tuning knobs of the launch configuration (a5).  Zero fields mean "library default".   */
@@ -172,7 +173,11 @@ typedef struct {
   int32_t xpencil_targets;   /* X-pencil: targets per consumer lane, 1 or 2 (default 1; 2
                                 reads each staged source once for two consecutive targets;
                                 the CANDIDATE test kernel always walks one)                 */
-  int32_t reserved[6];
+  int32_t exchange_full;     /* a8 (nranks > 1): 0 (default) = two-phase exchange, the counts
+                                first, then exactly the counted records (one stream
+                                synchronisation per exchange); 1 = the whole fixed-capacity
+                                messages, no host synchronisation (CUDA-graph capturable)     */
+  int32_t reserved[5];
 } pi_tuning;
 
 PI_API int32_t pi_abi_version(void);

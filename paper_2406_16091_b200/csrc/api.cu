@@ -377,6 +377,13 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
       pi_destroy(c);
       return PI_ENCCL;
     }
+    // pinned host slot for the exchanged counts (the two-phase exchange reads them back)
+    if ((e = cudaHostAlloc(reinterpret_cast<void **>(&S.hcnt), 4 * sizeof(long long), cudaHostAllocDefault)) !=
+        cudaSuccess) {
+      pi_status s = cuda_check(c, e, "pi_create pinned counts");
+      pi_destroy(c);
+      return s;
+    }
   }
   *out = c;
   return PI_OK;
@@ -399,6 +406,7 @@ pi_status pi_destroy(pi_ctx c) {
       cudaStreamDestroy(c->d2h);
     }
     delete c->slab.tr;
+    if (c->slab.hcnt) cudaFreeHost(c->slab.hcnt);
   }
   delete c;
   return PI_OK;
@@ -413,6 +421,7 @@ pi_status pi_set_stream(pi_ctx c, void *stream) {
 pi_status pi_set_tuning(pi_ctx c, const pi_tuning *t) {
   if (!c || !t) return PI_EINVAL;
   c->tune = *t;
+  c->slab.counted = t->exchange_full == 0;
   return PI_OK;
 }
 
@@ -462,7 +471,7 @@ static pi_status slab_ghosts_and_bin(pi_ctx c) {
   phase_begin(c, 2);
   if ((e = slab_reset(S, c->ctl, c->stream)) != cudaSuccess) return cuda_check(c, e, "slab reset");
   if ((e = slab_select_ghosts(S, c->g, cap, c->ctl, c->stream)) != cudaSuccess) return cuda_check(c, e, "ghosts");
-  if ((e = S.tr->exchange(S, c->stream)) != cudaSuccess) return fail(c, PI_ENCCL, "ghost exchange failed");
+  if ((e = slab_exchange(S, c->stream)) != cudaSuccess) return fail(c, PI_ENCCL, "ghost exchange failed");
   if ((e = slab_append(S, &c->ctl->n_owned, &c->ctl->n_total, &c->ctl->ghosts_in, &c->ctl->pad2[1], cap, c->ctl,
                        c->stream)) !=
       cudaSuccess)
@@ -585,7 +594,7 @@ pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
       if ((e = slab_reset(S, c->ctl, c->stream)) != cudaSuccess) return cuda_check(c, e, "slab reset");
       if ((e = slab_migrate(S, c->g, cap, c->rec, c->urec, c->uid, c->ctl, c->stream)) != cudaSuccess)
         return cuda_check(c, e, "migrate");
-      if ((e = S.tr->exchange(S, c->stream)) != cudaSuccess) return fail(c, PI_ENCCL, "migration exchange failed");
+      if ((e = slab_exchange(S, c->stream)) != cudaSuccess) return fail(c, PI_ENCCL, "migration exchange failed");
       if ((e = slab_append(S, &c->ctl->n_stay, &c->ctl->n_owned, &c->ctl->migrants_in, &c->ctl->migrants_out, cap,
                            c->ctl, c->stream)) !=
           cudaSuccess)
@@ -791,6 +800,7 @@ pi_status pi_get_stats(pi_ctx c, pi_stats *out) {
   out->candidates = (int64_t)cand;
   out->fallback_cells = (int64_t)h.fallback_cells;
   out->steps = c->steps;
+  out->exchange_bytes = c->slab.bytes_sent;
   for (int k = 0; k < 4; ++k) {
     float ms = 0.f;
     if (c->ev_used[k] && cudaEventElapsedTime(&ms, c->ev[k][0], c->ev[k][1]) == cudaSuccess) out->phase_ms[k] = ms;

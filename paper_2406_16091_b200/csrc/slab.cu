@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <algorithm>
+
 #include "slab.cuh"
 
 namespace pi {
@@ -240,19 +242,24 @@ struct LocalTransport : Transport {
       delete grp;
     }
   }
-  cudaError_t exchange(SlabState &S, cudaStream_t s) override {
+  cudaError_t run(SlabState &S, cudaStream_t s, const Xfer *L, int nL, const Xfer *R, int nR) override {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return e;
     if (!grp->barrier()) return cudaErrorTimeout;  // every rank's send buffers are complete
-    const size_t bytes = msg_bytes(S.cap_msg);
+    auto u8 = [](void *p, size_t o) { return static_cast<unsigned char *>(p) + o; };
     if (S.rank > 0) {
-      SlabState *L = grp->members[S.rank - 1];
-      if ((e = cudaMemcpyAsync(S.recvL, L->sendR, bytes, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return e;
+      SlabState *P = grp->members[S.rank - 1];
+      for (int k = 0; k < nL && e == cudaSuccess; ++k)
+        if (L[k].rbytes)
+          e = cudaMemcpyAsync(u8(S.recvL, L[k].off), u8(P->sendR, L[k].off), L[k].rbytes, cudaMemcpyDeviceToDevice, s);
     }
     if (S.rank < S.nranks - 1) {
-      SlabState *R = grp->members[S.rank + 1];
-      if ((e = cudaMemcpyAsync(S.recvR, R->sendL, bytes, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return e;
+      SlabState *P = grp->members[S.rank + 1];
+      for (int k = 0; k < nR && e == cudaSuccess; ++k)
+        if (R[k].rbytes)
+          e = cudaMemcpyAsync(u8(S.recvR, R[k].off), u8(P->sendL, R[k].off), R[k].rbytes, cudaMemcpyDeviceToDevice, s);
     }
+    if (e != cudaSuccess) return e;
     e = cudaStreamSynchronize(s);
     if (!grp->barrier()) return cudaErrorTimeout;  // nobody overwrites a send buffer still being read
     return e;
@@ -310,19 +317,21 @@ struct NcclTransport : Transport {
   ~NcclTransport() override {
     if (comm) g_nccl.destroy(comm);
   }
-  cudaError_t exchange(SlabState &S, cudaStream_t s) override {
-    const size_t bytes = msg_bytes(S.cap_msg);
+  cudaError_t run(SlabState &S, cudaStream_t s, const Xfer *L, int nL, const Xfer *R, int nR) override {
     constexpr int ncclChar = 0;
+    auto u8 = [](void *p, size_t o) { return static_cast<unsigned char *>(p) + o; };
     if (g_nccl.gstart() != 0) return cudaErrorUnknown;
     bool ok = true;
-    if (S.rank > 0) {
-      ok &= g_nccl.send(S.sendL, bytes, ncclChar, S.rank - 1, comm, s) == 0;
-      ok &= g_nccl.recv(S.recvL, bytes, ncclChar, S.rank - 1, comm, s) == 0;
-    }
-    if (S.rank < S.nranks - 1) {
-      ok &= g_nccl.send(S.sendR, bytes, ncclChar, S.rank + 1, comm, s) == 0;
-      ok &= g_nccl.recv(S.recvR, bytes, ncclChar, S.rank + 1, comm, s) == 0;
-    }
+    if (S.rank > 0)
+      for (int k = 0; k < nL; ++k) {
+        if (L[k].sbytes) ok &= g_nccl.send(u8(S.sendL, L[k].off), L[k].sbytes, ncclChar, S.rank - 1, comm, s) == 0;
+        if (L[k].rbytes) ok &= g_nccl.recv(u8(S.recvL, L[k].off), L[k].rbytes, ncclChar, S.rank - 1, comm, s) == 0;
+      }
+    if (S.rank < S.nranks - 1)
+      for (int k = 0; k < nR; ++k) {
+        if (R[k].sbytes) ok &= g_nccl.send(u8(S.sendR, R[k].off), R[k].sbytes, ncclChar, S.rank + 1, comm, s) == 0;
+        if (R[k].rbytes) ok &= g_nccl.recv(u8(S.recvR, R[k].off), R[k].rbytes, ncclChar, S.rank + 1, comm, s) == 0;
+      }
     ok &= g_nccl.gend() == 0;
     return ok ? cudaSuccess : cudaErrorUnknown;
   }
@@ -330,6 +339,32 @@ struct NcclTransport : Transport {
 };
 
 }  // namespace
+
+cudaError_t slab_exchange(SlabState &S, cudaStream_t s) {
+  const bool hasL = S.rank > 0, hasR = S.rank < S.nranks - 1;
+  if (!S.counted || !S.hcnt) {  // the whole fixed-capacity messages, no host synchronisation
+    const Xfer x{0, msg_bytes(S.cap_msg), msg_bytes(S.cap_msg)};
+    S.bytes_sent += (long long)x.sbytes * (hasL + hasR);
+    return S.tr->run(S, s, &x, hasL, &x, hasR);
+  }
+  // phase 1: the headers (counts)
+  const Xfer h{0, sizeof(MsgHeader), sizeof(MsgHeader)};
+  cudaError_t e = S.tr->run(S, s, &h, hasL, &h, hasR);
+  void *hd[4] = {S.sendL, S.sendR, S.recvL, S.recvR};
+  for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+    e = cudaMemcpyAsync(S.hcnt + k, hd[k], sizeof(long long), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  auto clampc = [&](long long v) { return (size_t)std::min(std::max(v, 0LL), S.cap_msg); };
+  const size_t sl = hasL ? clampc(S.hcnt[0]) : 0, sr = hasR ? clampc(S.hcnt[1]) : 0;
+  const size_t rl = hasL ? clampc(S.hcnt[2]) : 0, rr = hasR ? clampc(S.hcnt[3]) : 0;
+  // phase 2: rec[0, n) and id[0, n) of each message (k_append reads the counts from the headers)
+  const size_t o_rec = sizeof(MsgHeader), o_id = sizeof(MsgHeader) + (size_t)S.cap_msg * 16;
+  const Xfer L[2] = {{o_rec, sl * 16, rl * 16}, {o_id, sl * 4, rl * 4}};
+  const Xfer R[2] = {{o_rec, sr * 16, rr * 16}, {o_id, sr * 4, rr * 4}};
+  S.bytes_sent += (long long)((sl + sr) * 20 + sizeof(MsgHeader) * (hasL + hasR));
+  return S.tr->run(S, s, L, hasL ? 2 : 0, R, hasR ? 2 : 0);
+}
 
 bool nccl_unique_id(void *out128, char *why, size_t n) {
   if (!g_nccl.load(why, n)) return false;

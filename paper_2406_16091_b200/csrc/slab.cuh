@@ -7,8 +7,12 @@
 // whose new global cell left the slab MIGRATE to r-1 / r+1 (|dx| < w per step: reading C11);
 // then the first / last owned layers are sent as ghosts; owned + ghosts are binned together
 // (the ghosts land in the ghost layers) and only owned cells are targets, so no reduction is
-// needed.  Messages are fixed-capacity (count header + records), so the exchange needs no
-// host synchronisation and no variable-size handshake.
+// needed.  Messages are fixed-capacity buffers (count header + records).  The exchange runs in
+// two phases: the headers (the counts) first, then exactly the counted records
+// (rec[0, n) and id[0, n)), so the link carries the real payload, not the capacity; the counts
+// reach the host through a pinned buffer (one stream synchronisation per exchange).  With
+// counted = false the whole fixed-capacity message is sent and no host synchronisation is needed
+// (CUDA-graph capturable with the NCCL transport).
 #pragma once
 #include "pi_internal.cuh"
 
@@ -34,18 +38,32 @@ struct Transport;
 struct SlabState {
   int rank = 0, nranks = 1, Lx = 0;
   long long cap_msg = 0;
+  bool counted = true;           // two-phase exchange: headers, then exactly the counted records
+  long long *hcnt = nullptr;     // pinned host [4]: send L, send R, recv L, recv R counts
+  long long bytes_sent = 0;      // payload bytes this rank put on the links (host bookkeeping)
   void *sendL = nullptr, *sendR = nullptr, *recvL = nullptr, *recvR = nullptr;
   float4 *xrec = nullptr;  // owned (+ arrivals, + ghosts) records: input of the binning
   int32_t *xid = nullptr, *xperm = nullptr;
   Transport *tr = nullptr;
 };
 
+// One region of the messages moved between neighbours: bytes [off, off + sbytes) of this rank's
+// send buffer go to the neighbour, and [off, off + rbytes) of this rank's receive buffer are
+// filled from the neighbour's send buffer (the same layout on both sides).
+struct Xfer {
+  size_t off, sbytes, rbytes;
+};
+
 struct Transport {
   virtual ~Transport() {}
-  // sendL -> rank-1 (lands in its recvR), sendR -> rank+1 (its recvL); stream ordered.
-  virtual cudaError_t exchange(SlabState &S, cudaStream_t s) = 0;
+  // Grouped point-to-point: regions L[0..nL) with rank-1 (sendL -> its recvR, its sendR ->
+  // recvL) and R[0..nR) with rank+1; stream ordered.  Zero-byte sides are skipped (both ends
+  // agree: the sizes come from the same counts).
+  virtual cudaError_t run(SlabState &S, cudaStream_t s, const Xfer *L, int nL, const Xfer *R, int nR) = 0;
   virtual const char *name() const = 0;
 };
+// The a8 exchange of the current messages (both phases, see above).
+cudaError_t slab_exchange(SlabState &S, cudaStream_t s);
 
 // Creates the transport for cfg: "PILOCAL:<key>" ids link contexts of one process (testing on
 // one GPU), otherwise an NCCL communicator over cfg->nccl_unique_id (libnccl.so.2 is loaded

@@ -198,3 +198,46 @@ def test_slab_domain_flag():
     with cf.ThreadPoolExecutor(2) as pool:
         msgs = _all(pool, run, ctxs)
     assert all("flags 0x8" in m for m in msgs), msgs
+
+
+def test_slab_exchange_counted_bytes():
+    """The two-phase exchange (counts first, then exactly the counted records: SURVEY.md §8(e))
+    and the fixed-capacity one (exchange_full = 1) give the same state; the counted one puts only
+    the real payload on the links: 20 B per ghost / migrant + a 16-B header per message."""
+    c = synth.make_config("c0", n=4 * 4096)
+    g = c.grid
+    P = 4
+    F = celllist.interact(c.x, c.y, c.z, c.q, g)["out"][:, 1:]
+    dt = float(np.float32(0.5 * g.w / np.abs(F).max()))
+    out = {}
+    for full in (0, 1):
+        ctxs = _contexts(g, P, capacity=c.n)
+        parts = [_partition(c, k) for k in ctxs]
+
+        def run(r, k):
+            k.set_tuning(exchange_full=full)
+            idx = parts[r]
+            with torch.cuda.stream(k.stream):
+                k.bin(*(_dev(a[idx]) for a in (c.x, c.y, c.z, c.q)), id=_dev(idx.astype(np.int32)))
+                k.step("xpencil", dt)
+                p = k.get_particles()
+            k.stream.synchronize()
+            return {key: v.cpu().numpy() for key, v in p.items()}, k.stats()
+
+        with cf.ThreadPoolExecutor(P) as pool:
+            out[full] = _all(pool, run, ctxs)
+        for k in ctxs:
+            k.close()
+    for full in (0, 1):
+        ids = np.concatenate([s["id"] for s, _ in out[full]])
+        assert np.array_equal(np.sort(ids), np.arange(c.n))
+    for r in range(P):
+        (s0, st0), (s1, st1) = out[0][r], out[1][r]
+        o0, o1 = np.argsort(s0["id"]), np.argsort(s1["id"])
+        assert np.array_equal(s0["id"][o0], s1["id"][o1])
+        for key in ("x", "y", "z", "phi", "fx", "fy", "fz"):  # (sums in another order after the atomic scatter)
+            a, b = s0[key][o0].astype(np.float64), s1[key][o1].astype(np.float64)
+            assert np.allclose(a, b, rtol=1e-5, atol=1e-5 * np.abs(b).max()), key
+        nmsg = 3 * ((r > 0) + (r < P - 1))  # pi_bin's ghost exchange + the step's migration and ghosts
+        assert st0["exchange_bytes"] >= 20 * st0["migrants_out"] + 16 * nmsg
+        assert st0["exchange_bytes"] < st1["exchange_bytes"] / 2  # the counted records, not the capacity
