@@ -106,8 +106,12 @@ typedef enum {
  *   PI_A_XPENCIL : X-pencil (Alg. 5, §5.2), re-designed to stream the
  *                  9 neighbour pencils of a target pencil along X through shared memory.
  *   PI_A_AUTO    : the fastest measured strategy for the workload: the global-memory kernel
- *                  below 3 particles per cell (mean), the X-pencil above.                  */
-typedef enum { PI_A_GLOBAL = 0, PI_A_FULLLOAD = 1, PI_A_XPENCIL = 2, PI_A_AUTO = 3 } pi_algo;
+ *                  below 3 particles per cell (mean), the X-pencil above.
+ *   PI_A_XPREG   : X-pencil-reg (§5.3): the targets
+ *                  of a sub-box of cells in registers, the (By+2)(Bz+2) source X-pencils around
+ *                  it staged one after the other, the box's own records copied to shared memory
+ *                  from the registers.  Needs the sorted records (pi_bin / pi_step write them).  */
+typedef enum { PI_A_GLOBAL = 0, PI_A_FULLLOAD = 1, PI_A_XPENCIL = 2, PI_A_AUTO = 3, PI_A_XPREG = 4 } pi_algo;
 
 typedef struct {
   /* Global grid (PAPER.md:54-56 §2, :93 §3).  Cells are cubes of width cell_width; the box

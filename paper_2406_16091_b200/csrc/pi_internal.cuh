@@ -276,5 +276,6 @@ inline cudaError_t allow_max_smem(F *func) {
 cudaError_t launch_interact_global(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
+cudaError_t launch_interact_xpreg(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 
 }  // namespace pi

@@ -50,7 +50,7 @@ def _dev(a):
 
 
 @pytest.mark.parametrize("P", [2, 4])
-@pytest.mark.parametrize("algo", ["global", "xpencil", "fullload"])
+@pytest.mark.parametrize("algo", ["global", "xpencil", "fullload", "xpreg"])
 def test_slab_bin_interact_matches_whole_cloud(P, algo):
     c = synth.make_config("c0", n=4 * 4096)
     g = c.grid

@@ -22,7 +22,7 @@ def state(ctx):
 @pytest.mark.parametrize("algo,kernel,xs,tune", [("global", "gaussian", 0, None), ("xpencil", "gaussian", 0, None),
                                                   ("fullload", "gaussian", 0, None), ("xpencil", "gaussian", 1, None),
                                                   ("xpencil", "gaussian", 8, None), ("xpencil", "lj", 0, None),
-                                                  ("global", "lj", 4, None),
+                                                  ("global", "lj", 4, None), ("xpreg", "gaussian", 2, None),
                                                   # every cell through the Par-Cell-SM pass
                                                   ("xpencil", "gaussian", 0, dict(xpencil_cap=16)),
                                                   ("xpencil", "lj", 2, dict(xpencil_cap=16))])
