@@ -339,6 +339,34 @@ def side_config(a, dev, stream, flush, name):
             "interact_ms": statistics.median(ims), "unit": "candidate pair interactions/s"}
 
 
+def strategies_at(a, dev, stream, name="c1"):
+    """pi_interact of every strategy on one config (device time, candidate pairs/s): the paper's
+    strategy comparison (Table 1 / Fig. perf) incl. X-pencil-reg (NEXT #1)."""
+    import torch
+    import synth
+    from paper_2406_16091_b200 import Context
+    c = synth.make_config(name)
+    g = c.grid
+    ctx = Context(g.dims, g.w, g.r_c, g.origin, capacity=c.n, device=dev, stream=stream)
+    x, y, z, q = (torch.from_numpy(v).to(dev) for v in (c.x, c.y, c.z, c.q))
+    ctx.bin(x, y, z, q)
+    out = {"workload": WORKLOADS.get(name, name), "unit": "candidate pair interactions/s"}
+    for algo in ("global", "fullload", "xpencil", "xpreg"):
+        ctx.interact(algo, out=False)
+        ms = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.interact(algo, out=False)
+            e1.record(stream)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        m = statistics.median(ms)
+        out[algo] = {"interact_ms": m, "value": ctx.stats()["candidates"] / (m * 1e-3)}
+    ctx.close()
+    return out
+
+
 def hbm_peak_gbs():
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -583,6 +611,8 @@ def run_ours(a):
         line["binning_2e24"] = binning_at_scale(a, dev, stream, flush)
     if world == 1 and not a.no_c1 and a.config != "c1":
         line["config_c1"] = side_config(a, dev, stream, flush, "c1")
+    if world == 1 and not a.no_c1:
+        line["strategies_c1"] = strategies_at(a, dev, stream, "c1")
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

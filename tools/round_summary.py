@@ -62,20 +62,23 @@ out = [f"# {R}: ncu summaries (B200, `--set full --clock-control none`, one capt
        "Durations under ncu are serialised and cold-cache: compare shares, not absolute times (bench.py",
        "times the kernels live with CUDA events).\n"]
 traffic, smem = {}, {}
-for name, title in (("xpencil", "X-pencil interaction (configs[1], 2^21, 64^3)"),
+for name, title in (("xpencil_c4", "X-pencil interaction, the bench kernel (configs[4], 2^27, 256^3)"),
+                    ("xpencil", "X-pencil interaction (configs[1], 2^21, 64^3)"),
                     ("global", "global-memory baseline PPNL (configs[1])"),
-                    ("fullload", "full-load interaction (configs[1])")):
+                    ("fullload", "full-load interaction (configs[1])"),
+                    ("xpreg", "X-pencil-reg interaction (configs[1])")):
     rep = os.path.join(G, f"{R}_{name}.ncu-rep")
     if not os.path.exists(rep):
         continue
     for d in raw(rep):
         s, tr = fmt(d)
         out.append(f"## {title}: `{d['Kernel Name'][:60]}`\n{s}\n")
-        traffic[name] = int(tr)
+        key = "xpencil" if name == "xpencil_c4" else (name + "_c1" if name == "xpencil" else name)
+        traffic[key] = int(tr)
         w = d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")
         if w not in (None, ""):
-            smem[name] = round(float(w) / 100.0, 4)
-for name, title in (("rebin", "binning, pi_step delta re-binning at 2^24 (configs[2] ppc 8: scan of the carried counts + scatter of the nearly sorted records)"),
+            smem[key] = round(float(w) / 100.0, 4)
+for name, title in (("rebin", "binning, pi_step delta re-binning on configs[4] (2^27: scan of the carried counts + scatter of the nearly sorted records)"),
                     ("bin", "binning, pi_bin at 2^24 (configs[2] ppc 8, random input order)")):
     rep = os.path.join(G, f"{R}_{name}.ncu-rep")
     if not os.path.exists(rep):
@@ -97,7 +100,8 @@ if os.path.exists(ll):
         tot[k] += float(r[iV])
         cnt[k] += 1
     s = sum(tot.values())
-    out.append("## Launch list of `bench.py --steps 3 --warmup 3 --no-binning-2e24` (all kernels of the run, ncu-serialised)\n")
+    out.append("## Launch list of `bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-binning-2e24 --no-c1` "
+               "(configs[4]; all kernels of the run, ncu-serialised)\n")
     out.append("| kernel | launches | total us | share |\n|---|---|---|---|")
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
         out.append(f"| `{k}` | {cnt[k]} | {v / 1e3:.1f} | {100 * v / s:.1f} % |")
