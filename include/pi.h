@@ -135,7 +135,8 @@ typedef struct {
                                 particles are ordered by sub-cell floor(sx (t - c)), t the
                                 contract's scaled coordinate (R18), so the X-pencil
                                 can skip sources farther than r_c along X; 1, 2, 4, 8 or 16
-                                (0 -> 2).  Counts, offsets and M_C stay per cell.            */
+                                (0 -> 4: configs[4] step 19.9 -> 19.4 ms against 2, r02).
+                                Counts, offsets and M_C stay per cell.                       */
   int32_t reserved[7];       /* must be zero                                                 */
 } pi_config;
 

@@ -55,7 +55,7 @@ SlabGeom slab_geom(const pi_config *cfg) {
   return s;
 }
 
-int x_subcells(const pi_config *cfg) { return cfg->x_subcells > 0 ? cfg->x_subcells : 2; }
+int x_subcells(const pi_config *cfg) { return cfg->x_subcells > 0 ? cfg->x_subcells : 4; }
 
 Layout make_layout(const pi_config *cfg) {
   const SlabGeom sg = slab_geom(cfg);
@@ -226,7 +226,7 @@ static bool config_ok(const pi_config *cfg, char *why, size_t n) {
   // the fine (X sub-cell) index is 32-bit arithmetic in the kernels; with nranks > 1
   // the local grid has two extra X layers
   const long long lx = cfg->dims[0] / cfg->nranks + (cfg->nranks > 1 ? 2 : 0);
-  if (lx * cfg->dims[1] * cfg->dims[2] * (cfg->x_subcells > 0 ? cfg->x_subcells : 2) >= (1LL << 31) - 1) {
+  if (lx * cfg->dims[1] * cfg->dims[2] * x_subcells(cfg) >= (1LL << 31) - 1) {
     snprintf(why, n, "cells x x_subcells must stay below 2^31");
     return false;
   }
