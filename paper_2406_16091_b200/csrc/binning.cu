@@ -35,45 +35,7 @@ constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;  // 4096 cells per tile
 static_assert(SCAN_TILE == (1 << SCAN_TILE_SHIFT), "scan tile");
 
 // a1 + a2 over SoA input (pi_bin, arbitrary order): 4 particles per thread through float4
-// loads, one plain atomic per particle (lanes of random-order input rarely share a cell).
-__global__ void __launch_bounds__(COUNT_THREADS) k_count_soa(long long n, const float *__restrict__ x,
-                                                              const float *__restrict__ y,
-                                                              const float *__restrict__ z, Geom g,
-                                                              int32_t *__restrict__ counts, DevCtl *ctl) {
-  const long long nvec = (n + 3) >> 2;
-  bool bad = false;
-  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
-       v += (long long)gridDim.x * blockDim.x) {
-    const long long i0 = v << 2;
-    float xs[4], ys[4], zs[4];
-    if (i0 + 3 < n) {
-      const float4 a = __ldg(reinterpret_cast<const float4 *>(x) + v);
-      const float4 b = __ldg(reinterpret_cast<const float4 *>(y) + v);
-      const float4 c = __ldg(reinterpret_cast<const float4 *>(z) + v);
-      xs[0] = a.x; xs[1] = a.y; xs[2] = a.z; xs[3] = a.w;
-      ys[0] = b.x; ys[1] = b.y; ys[2] = b.z; ys[3] = b.w;
-      zs[0] = c.x; zs[1] = c.y; zs[2] = c.z; zs[3] = c.w;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool ok = i0 + j < n;
-        xs[j] = ok ? x[i0 + j] : 0.f;
-        ys[j] = ok ? y[i0 + j] : 0.f;
-        zs[j] = ok ? z[i0 + j] : 0.f;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (i0 + j >= n) break;
-      bool b = false;
-      const int lin = fine_lin(g, xs[j], ys[j], zs[j], b);
-      bad |= b;
-      atomicAdd(counts + lin, 1);
-    }
-  }
-  if (bad) atomicOr(&ctl->flags, FLAG_OUT_OF_BOX);
-}
-
+// loads, warp-aggregated atomics (one per distinct (sub-)cell among the warp's lanes).
 // Runs of equal cells among consecutive lanes (the nearly sorted AoS input): one atomic per
 // run.  Returns the run's first lane and length for this lane (invalid lanes: runs of one).
 __device__ __forceinline__ void lane_run(int lin, bool valid, int &head, int &len) {
@@ -93,6 +55,51 @@ __device__ __forceinline__ void run_count(int32_t *counts, int lin, bool valid) 
   int head, len;
   lane_run(lin, valid, head, len);
   if (valid && (int)(threadIdx.x & 31) == head) atomicAdd(counts + lin, len);
+}
+
+__global__ void __launch_bounds__(COUNT_THREADS) k_count_soa(long long n, const float *__restrict__ x,
+                                                              const float *__restrict__ y,
+                                                              const float *__restrict__ z, Geom g,
+                                                              int32_t *__restrict__ counts, DevCtl *ctl) {
+  const long long nvec = (n + 3) >> 2;
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+  // whole warps iterate together (the run aggregation shuffles over all 32 lanes)
+  for (long long vb = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); vb < nvec;
+       vb += (long long)gridDim.x * blockDim.x) {
+    const long long v = vb + lane;
+    const long long i0 = v << 2;
+    float xs[4] = {0.f, 0.f, 0.f, 0.f}, ys[4] = {0.f, 0.f, 0.f, 0.f}, zs[4] = {0.f, 0.f, 0.f, 0.f};
+    if (i0 + 3 < n) {
+      const float4 a = __ldg(reinterpret_cast<const float4 *>(x) + v);
+      const float4 b = __ldg(reinterpret_cast<const float4 *>(y) + v);
+      const float4 c = __ldg(reinterpret_cast<const float4 *>(z) + v);
+      xs[0] = a.x; xs[1] = a.y; xs[2] = a.z; xs[3] = a.w;
+      ys[0] = b.x; ys[1] = b.y; ys[2] = b.z; ys[3] = b.w;
+      zs[0] = c.x; zs[1] = c.y; zs[2] = c.z; zs[3] = c.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool ok = i0 + j < n;
+        xs[j] = ok ? x[i0 + j] : 0.f;
+        ys[j] = ok ? y[i0 + j] : 0.f;
+        zs[j] = ok ? z[i0 + j] : 0.f;
+      }
+    }
+    // warp-aggregated atomics (north star step 2): one atomicAdd per run of equal (sub-)cells
+    // among consecutive lanes (particle j of lane l and of lane l + 1 are 4 apart in the input):
+    // cell-ordered or clustered input adds whole runs at once, random order costs a shuffle and
+    // a ballot per particle
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool valid = i0 + j < n;
+      bool b = false;
+      const int lin = valid ? fine_lin(g, xs[j], ys[j], zs[j], b) : -1;
+      bad |= b;
+      run_count(counts, lin, valid);
+    }
+  }
+  if (bad) atomicOr(&ctl->flags, FLAG_OUT_OF_BOX);
 }
 
 // Scatter of the AoS path: a distinct rank in [0, count) per particle, taken from the counts

@@ -118,3 +118,13 @@ def test_partitioned_buckets_with_ids(kind):
     _, _, _, perm = ctx.get_binning()
     parts = ctx.get_particles()
     assert np.array_equal(parts["id"].cpu().numpy(), ids[perm.cpu().numpy()])
+
+
+def test_cell_sorted_input():
+    """pi_bin of input already in cell order (lanes of a warp share cells: the count's
+    warp-aggregated atomics add whole runs at once) bins bit-exactly too."""
+    c = synth.make_config("c1")
+    cells = celllist.cells(c.x, c.y, c.z, c.grid)
+    order = np.argsort(cells, kind="stable")
+    s = synth.Cloud(c.grid, c.x[order], c.y[order], c.z[order], c.q[order])
+    check_binning(s)
