@@ -406,13 +406,10 @@ def run_ours(a):
     ctx = make_ctx()
     x, y, z, q = (torch.from_numpy(v).to(dev) for v in (cloud.x, cloud.y, cloud.z, cloud.q))
 
-    # cutoff pairs P (INDICATOR kernel, q = 1) for the algorithmic FLOP count 8 C + 10 P
-    ci = make_ctx("indicator")
-    ci.bin(x, y, z, torch.ones_like(q))
-    phi, *_ = ci.interact("global")
-    P = float(phi.double().sum().item())
-    ci.close()
-    del ci, phi
+    # cutoff pairs P of this rank's targets (pi_count_pairs: the global baseline's walk over the
+    # sorted state) for the algorithmic FLOP count 8 C + 10 P of this rank's interaction kernel
+    ctx.bin(x, y, z, q)
+    P = float(ctx.count_pairs())
 
     # dt: max |dt F| <= 0.01 w, the same on every rank
     ctx.bin(x, y, z, q)

@@ -278,6 +278,13 @@ PI_API pi_status pi_get_particles(pi_ctx ctx, float *x, float *y, float *z, floa
 /* Synchronises the stream and fills *out.  Returns PI_EDEVICE if a sticky flag is set.      */
 PI_API pi_status pi_get_stats(pi_ctx ctx, pi_stats *out);
 
+/* P, the statistic of SURVEY.md §5 beside C: the ordered pairs (i, j), j != i, with r_ij < r_c
+ * (strict) over this rank's owned targets in the current sorted state (the state
+ * the last interaction used), counted by a separate pass with the global baseline's walk and
+ * fp32 arithmetic -- the interaction kernels do not count it (it would cost the hot loop).
+ * *pairs: host int64.  Synchronises.  Errors: PI_EINVAL (NULL), PI_ESTATE (before pi_bin).    */
+PI_API pi_status pi_count_pairs(pi_ctx ctx, int64_t *pairs);
+
 PI_API const char *pi_last_error(pi_ctx ctx);
 
 #ifdef __cplusplus

@@ -238,6 +238,12 @@ class Context:
                                                _ptr(fx), _ptr(fy), _ptr(fz)))
         return dict(x=x, y=y, z=z, q=q, id=ids, phi=phi, fx=fx, fy=fy, fz=fz)
 
+    def count_pairs(self):
+        """P: cutoff pairs of the owned targets in the current sorted state (pi_count_pairs)."""
+        v = ctypes.c_int64(0)
+        self._check(self._lib.pi_count_pairs(self._h, ctypes.byref(v)))
+        return int(v.value)
+
     def stats(self, check=True):
         s = L.pi_stats()
         st = self._lib.pi_get_stats(self._h, ctypes.byref(s))

@@ -57,6 +57,7 @@ SIGNATURES = {
     "pi_get_binning": (ctypes.c_int, [P, P, P, P, P]),
     "pi_get_particles": (ctypes.c_int, [P, P, P, P, P, P, P, P, P, P]),
     "pi_get_stats": (ctypes.c_int, [P, ctypes.POINTER(pi_stats)]),
+    "pi_count_pairs": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_int64)]),
     "pi_last_error": (ctypes.c_char_p, [P]),
 }
 

@@ -810,6 +810,28 @@ pi_status pi_get_stats(pi_ctx c, pi_stats *out) {
   return PI_OK;
 }
 
+pi_status pi_count_pairs(pi_ctx c, int64_t *pairs) {
+  if (!c || !pairs) return PI_EINVAL;
+  if (c->state == 0) return fail(c, PI_ESTATE, "pi_count_pairs before pi_bin");
+  if (!c->rec_ok && !c->pairs_ready) return fail(c, PI_ESTATE, "pi_count_pairs: no sorted state");
+  const bool multi = c->cfg.nranks > 1;
+  InteractArgs a{};
+  a.n = multi ? c->cfg.capacity : c->n;
+  a.n_dev = multi ? &c->ctl->n_total : nullptr;
+  a.rec = c->rec_ok ? c->rec : nullptr;
+  a.pairs = c->pairs;
+  a.pair_plane = pair_plane_of(c->cfg.capacity);
+  a.offsets = c->offsets;
+  a.ctl = c->ctl;
+  cudaError_t e = launch_count_pairs(c->g, c->kp, a, c->stream);
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, &c->ctl->pairs, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_check(c, e, "pi_count_pairs");
+  *pairs = (int64_t)h;
+  return PI_OK;
+}
+
 const char *pi_last_error(pi_ctx c) { return c ? c->err : "NULL context"; }
 
 }  // extern "C"

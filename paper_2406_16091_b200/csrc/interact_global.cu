@@ -91,7 +91,55 @@ __global__ void __launch_bounds__(PPNL_THREADS) k_interact_global(long long n, c
   if ((threadIdx.x & 31) == 0 && cand) atomicAdd(&ctl->cand_slots[(blockIdx.x * 4 + (threadIdx.x >> 5)) & (CAND_SLOTS - 1)], cand);
 }
 
+// P (SURVEY.md §5 statistics): the cutoff pairs of the current sorted state, counted with the
+// global baseline's walk and arithmetic (r^2 of the fp32 differences, strict r < r_c).
+__global__ void __launch_bounds__(PPNL_THREADS) k_count_pairs(long long n, const float4 *__restrict__ rec,
+                                                              const float4 *__restrict__ pairs, long long plane,
+                                                              const int32_t *__restrict__ offsets, Geom g, float rc2,
+                                                              DevCtl *ctl, const long long *n_dev) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n_dev) n = *n_dev;
+  unsigned long long cnt = 0;
+  if (t < n) {
+    const float4 me = sorted_rec(rec, pairs, plane, (int)t);
+    bool bad = false;
+    const int cx = cell_x(g, me.x, bad);
+    if (cx >= g.own_lo && cx < g.own_hi) {
+      const int cy = cell_coord(me.y, g.oy, g.inv_w, g.ny, bad);
+      const int cz = cell_coord(me.z, g.oz, g.inv_w, g.nz, bad);
+      const int xlo = max(cx - 1, 0), xhi = min(cx + 1, g.nx - 1);
+      for (int dz = -1; dz <= 1; ++dz) {
+        const int z = cz + dz;
+        if (z < 0 || z >= g.nz) continue;
+        for (int dy = -1; dy <= 1; ++dy) {
+          const int y = cy + dy;
+          if (y < 0 || y >= g.ny) continue;
+          const long long row = (long long)g.nx * (y + (long long)g.ny * z);
+          const int lo = __ldg(offsets + row + xlo), hi = __ldg(offsets + row + xhi + 1);
+          for (int s = lo; s < hi; ++s) {
+            if (s == t) continue;
+            const float4 o = sorted_rec(rec, pairs, plane, s);
+            const float dx = me.x - o.x, dy2 = me.y - o.y, dz2 = me.z - o.z;
+            cnt += fmaf(dz2, dz2, fmaf(dy2, dy2, dx * dx)) < rc2;
+          }
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctl->pairs, cnt);
+}
+
 }  // namespace
+
+cudaError_t launch_count_pairs(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(&a.ctl->pairs, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess || a.n <= 0) return e;
+  const int blocks = (int)((a.n + PPNL_THREADS - 1) / PPNL_THREADS);
+  k_count_pairs<<<blocks, PPNL_THREADS, 0, s>>>(a.n, a.rec, a.pairs, a.pair_plane, a.offsets, g, k.rc2, a.ctl,
+                                                a.n_dev);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_interact_global(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s) {
   if (a.n <= 0) return cudaSuccess;

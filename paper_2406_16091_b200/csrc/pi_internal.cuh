@@ -56,6 +56,7 @@ struct DevCtl {
   unsigned long long pad[4];         // X-pencil dense cells: listed [0], Par-Cell-SM ticket [1],
                                       // blocks whose producer finished [2]
   unsigned long long cand_slots[64];  // candidates (C) of the last interaction, spread counters
+  unsigned long long pairs;           // cutoff pairs (P) counted by pi_count_pairs
 };
 constexpr int CAND_SLOTS = 64;
 
@@ -277,5 +278,7 @@ cudaError_t launch_interact_global(const Geom &g, const KParams &k, const Intera
 cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 cudaError_t launch_interact_xpreg(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
+// P: ordered pairs (i, j), j != i, r_ij < r_c, over the owned targets of the sorted state -> ctl->pairs
+cudaError_t launch_count_pairs(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 
 }  // namespace pi

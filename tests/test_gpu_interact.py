@@ -335,3 +335,19 @@ def test_cost_sweep_kernels(algo, kernel, ppc):
                       np.array([1.5], np.float32))
     got, _ = gpu_interact(one, algo, kernel)
     assert np.all(got == 0)
+
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_count_pairs(name):
+    """pi_count_pairs (P) equals the oracle's sum of P_i, after pi_bin (records) and
+    after a pi_step that left only the source-pair array of the re-binned state.  Exact up to the
+    pairs inside the fp32/fp64 ambiguity band (R15), counted by the oracle (q = 1: A_i[0])."""
+    c = synth.make_config(name, qkind="ones")
+    ctx = ctx_for(c)
+    ctx.bin(*to_dev(c))
+    want = oracle_interact(c, "indicator")
+    P, amb = int(want["P"].sum()), int(want["A"][:, 0].sum())
+    assert abs(ctx.count_pairs() - P) <= amb
+    ctx.step("xpencil", 0.0)
+    ctx.step("xpencil", 0.0)    # dt = 0: the re-binned state (pair array only) is the same cloud
+    assert abs(ctx.count_pairs() - P) <= amb
