@@ -79,6 +79,23 @@ def test_workspace_bytes_validation(lib):
         c = _cfg()
         c.x_subcells = bad
         assert lib.pi_workspace_bytes(ctypes.byref(c)) == 0
+    # the fine (X sub-cell) index is 32-bit in the kernels: cells x x_subcells must stay < 2^31
+    # (ADVICE r01); 1024^3 cells with 4 sub-cells is refused, 512^3 with 8 accepted
+    big = _cfg(dims=(1024, 1024, 1024))
+    assert lib.pi_workspace_bytes(ctypes.byref(big)) == 0
+    ok8 = _cfg(dims=(512, 512, 512))
+    ok8.x_subcells = 8
+    assert lib.pi_workspace_bytes(ctypes.byref(ok8)) > 0
+    ok8.x_subcells = 16
+    assert lib.pi_workspace_bytes(ctypes.byref(ok8)) == 0
+    # every kernel id 0..5 (the cost sweep's LOWFLOP / HIGHFLOP included), nothing above
+    for k in range(6):
+        c = _cfg()
+        c.kernel = k
+        assert lib.pi_workspace_bytes(ctypes.byref(c)) > 0
+    c = _cfg()
+    c.kernel = 6
+    assert lib.pi_workspace_bytes(ctypes.byref(c)) == 0
 
 
 def test_create_rejects_bad_arguments_without_gpu(lib):

@@ -351,3 +351,31 @@ def test_count_pairs(name):
     ctx.step("xpencil", 0.0)
     ctx.step("xpencil", 0.0)    # dt = 0: the re-binned state (pair array only) is the same cloud
     assert abs(ctx.count_pairs() - P) <= amb
+
+
+def test_xpencil_fine_subcells_wide_grid():
+    """x_subcells = 16 on a grid 256 cells wide at 1-2 particles per cell: the X-pencil's segment
+    is sized from the shared-memory budget too (it used to need more than 227 KB for
+    its tables alone and returned PI_EINAPPLICABLE)."""
+    c = synth.scaled_uniform(1.5, (256, 8, 8), seed=240616099)
+    want = oracle_interact(c)
+    got, ctx = gpu_interact(c, "xpencil", ctx=ctx_for(c, x_subcells=16))
+    assert_parity(got, want, label="sx16 wide")
+    assert ctx.stats()["candidates"] == int(want["C"].sum())
+
+
+def test_run_host_after_submits():
+    """pi_run_host while pipelined runs are in flight drains them first (it shares
+    their I/O set 0): every run's host output is the oracle's."""
+    clouds = [synth.scaled_uniform(8, (12, 10, 9), seed=s) for s in (31, 32, 33)]
+    wants = [oracle_interact(c) for c in clouds]
+    ctx = ctx_for(clouds[0], capacity=max(c.n for c in clouds))
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    hin = [[pin(a) for a in (c.x, c.y, c.z, c.q)] for c in clouds]
+    hout = [[torch.full((c.n,), float("nan")).pin_memory() for _ in range(4)] for c in clouds]
+    ctx.run_host_submit("xpencil", *hin[0], *hout[0])
+    ctx.run_host_submit("xpencil", *hin[1], *hout[1])
+    ctx.run_host("xpencil", *hin[2], *hout[2])   # no wait in between
+    ctx.run_host_wait()
+    for k in range(3):
+        assert_parity(torch.stack(hout[k], 1).numpy(), wants[k], label=f"run {k}")
