@@ -182,7 +182,11 @@ typedef struct {
                                 first, then exactly the counted records (one stream
                                 synchronisation per exchange); 1 = the whole fixed-capacity
                                 messages, no host synchronisation (CUDA-graph capturable)     */
-  int32_t reserved[5];
+  int32_t xpencil_layout;    /* X-pencil staging: 0 (default) = the 9 pencils back to back (9
+                                runs per target; xpencil_targets applies); 1 = X-sub-cell-
+                                interleaved (a target's candidates are one contiguous range,
+                                one thread per target pair; measured slower)     */
+  int32_t reserved[4];
 } pi_tuning;
 
 PI_API int32_t pi_abi_version(void);

@@ -35,7 +35,7 @@ class pi_tuning(ctypes.Structure):
     _fields_ = [("xpencil_len", ctypes.c_int32), ("xpencil_cap", ctypes.c_int32),
                 ("fullload_box", ctypes.c_int32 * 3), ("fullload_cap", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("xpencil_slots", ctypes.c_int32), ("xpencil_targets", ctypes.c_int32),
-                ("exchange_full", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("exchange_full", ctypes.c_int32), ("xpencil_layout", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
 
 P = ctypes.c_void_p

@@ -453,9 +453,11 @@ static pi_status do_bin(pi_ctx c, long long n, const float *x, const float *y, c
   a.sid_out = c->sid;
   a.perm_out = (rec_in && !perm_in) ? nullptr : c->perm;
   a.perm_in = perm_in;
-  a.pairs_out = rec_in ? c->pairs : nullptr;
+  // the f32x2 source-pair array is read only by the X-pencil's pencil-by-pencil layout (the
+  // default; the interleaved layout, xpencil_layout = 1, stages records)
+  a.pairs_out = (rec_in && c->tune.xpencil_layout != 1) ? c->pairs : nullptr;
   a.pair_plane = pair_plane_of(c->cfg.capacity);
-  c->pairs_ready = rec_in != nullptr;
+  c->pairs_ready = a.pairs_out != nullptr;
   a.ctl = c->ctl;
   phase_begin(c, 0);
   cudaError_t e = launch_bin(c->g, a, c->stream);
@@ -522,7 +524,8 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.n = multi ? c->cfg.capacity : c->n;
   a.n_dev = multi ? &c->ctl->n_total : nullptr;
   a.n_est = multi ? c->n * (long long)(c->slab.Lx + 2) / (c->slab.Lx > 0 ? c->slab.Lx : 1) : c->n;
-  if (!c->rec_ok && algo != PI_A_XPENCIL && algo != PI_A_AUTO)
+  const bool r01_layout = (algo == PI_A_XPENCIL || algo == PI_A_AUTO) && c->tune.xpencil_layout != 1;
+  if (!c->rec_ok && !r01_layout)
     return fail(c, PI_ESTATE, "internal: sorted records not materialised for this strategy");
   a.rec = c->rec_ok ? c->rec : nullptr;
   a.foffsets = c->foffsets;
@@ -558,7 +561,10 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   phase_begin(c, 1);
   switch (algo) {
     case PI_A_GLOBAL: e = launch_interact_global(c->g, c->kp, a, c->stream); break;
-    case PI_A_XPENCIL: e = launch_interact_xpencil(c->g, c->kp, a, c->stream); break;
+    case PI_A_XPENCIL:
+      e = c->tune.xpencil_layout == 1 ? launch_interact_xpencil2(c->g, c->kp, a, c->stream)
+                                      : launch_interact_xpencil(c->g, c->kp, a, c->stream);
+      break;
     case PI_A_FULLLOAD: e = launch_interact_fullload(c->g, c->kp, a, c->stream); break;
     case PI_A_XPREG: e = launch_interact_xpreg(c->g, c->kp, a, c->stream); break;
     default: return fail(c, PI_EINVAL, "unknown algo %d", (int)algo);
@@ -605,7 +611,7 @@ pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
     } else {
       // the X-pencil reads only the pair array: the records need not be written (16 B/particle)
       s = do_bin(c, c->n, nullptr, nullptr, nullptr, nullptr, c->uid, c->urec, nullptr, nullptr, c->pcounts_ok,
-                 algo == PI_A_XPENCIL || algo == PI_A_AUTO);
+                 (algo == PI_A_XPENCIL || algo == PI_A_AUTO) && c->tune.xpencil_layout != 1);
     }
     if (s != PI_OK) return s;
   }

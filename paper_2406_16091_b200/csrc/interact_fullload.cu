@@ -48,81 +48,6 @@ __host__ __device__ inline size_t fl_smem_bytes(int bx, int by, int bz, int cap)
   return 16 + (size_t)fl_int_words(bx, by, bz) * 4 + (size_t)cap * 16;
 }
 
-struct TgtPair {
-  p2 x, y, z;
-};
-
-// One source (scalar broadcast) against the thread's two targets: 12 packed ops, 2 MUFU.
-template <int KERNEL>
-__device__ __forceinline__ void tp_eval(const TgtPair &t, const float4 a, const float thr, const float mc2, p2 &phi,
-                                        p2 &fx, p2 &fy, p2 &fz, const KParams &kp) {
-  if (KERNEL == PI_K_CANDIDATE) {
-    phi = add2(phi, pk(a.w));
-    return;
-  }
-  const p2 dx = add2(t.x, pk(-a.x));  // d = x_t - x_s
-  const p2 dy = add2(t.y, pk(-a.y));
-  const p2 dz = add2(t.z, pk(-a.z));
-  p2 r2 = mul2(dx, dx);
-  r2 = fma2(dy, dy, r2);
-  r2 = fma2(dz, dz, r2);
-  if (KERNEL == PI_K_GAUSSIAN) {
-    const p2 arg = mul2(r2, pk(mc2));
-    const float k0 = (lo(r2) < thr) ? ex2_approx(lo(arg)) : 0.f;
-    const float k1 = (hi(r2) < thr) ? ex2_approx(hi(arg)) : 0.f;
-    const p2 w = mul2(pk(k0, k1), pk(a.w));
-    phi = add2(phi, w);
-    fx = fma2(w, dx, fx);
-    fy = fma2(w, dy, fy);
-    fz = fma2(w, dz, fz);
-  } else if (kern_lj(KERNEL)) {
-    p2 w, wf;
-    lj_core<KERNEL>(r2, pk(a.w), thr, kp, w, wf);
-    phi = add2(phi, w);
-    fx = fma2(wf, dx, fx);
-    fy = fma2(wf, dy, fy);
-    fz = fma2(wf, dz, fz);
-  } else if (KERNEL == PI_K_LOWFLOP) {  // selects (an inert partner is at 1e30)
-    const bool i0 = lo(r2) < thr, i1 = hi(r2) < thr;
-    const float sm = lf_sum(a.x, a.y, a.z);
-    phi = add2(phi, pk(i0 ? sm : 0.f, i1 ? sm : 0.f));
-    fx = add2(fx, pk(i0 ? a.x : 0.f, i1 ? a.x : 0.f));
-    fy = add2(fy, pk(i0 ? a.y : 0.f, i1 ? a.y : 0.f));
-    fz = add2(fz, pk(i0 ? a.z : 0.f, i1 ? a.z : 0.f));
-  } else {
-    phi = add2(phi, pk((lo(r2) < thr) ? a.w : 0.f, (hi(r2) < thr) ? a.w : 0.f));
-  }
-}
-
-// The exact phi term added for target half h against itself (d = 0: no force term).
-template <int KERNEL>
-__device__ __forceinline__ float tp_self(const TgtPair &t, int h, const float4 a, const float thr, const float mc2,
-                                         const KParams &kp) {
-  if (KERNEL == PI_K_CANDIDATE) return a.w;
-  if (KERNEL == PI_K_LOWFLOP) return lf_sum(a.x, a.y, a.z);
-  if (kern_lj(KERNEL)) {  // the same lj_core operations as tp_eval, this half
-    const p2 dx = add2(t.x, pk(-a.x));
-    const p2 dy = add2(t.y, pk(-a.y));
-    const p2 dz = add2(t.z, pk(-a.z));
-    p2 r2 = mul2(dx, dx);
-    r2 = fma2(dy, dy, r2);
-    r2 = fma2(dz, dz, r2);
-    p2 w, wf;
-    lj_core<KERNEL>(r2, pk(a.w), thr, kp, w, wf);
-    return h ? hi(w) : lo(w);
-  }
-  const p2 dx = add2(t.x, pk(-a.x));
-  const p2 dy = add2(t.y, pk(-a.y));
-  const p2 dz = add2(t.z, pk(-a.z));
-  p2 r2 = mul2(dx, dx);
-  r2 = fma2(dy, dy, r2);
-  r2 = fma2(dz, dz, r2);
-  const p2 arg = mul2(r2, pk(mc2));
-  const float rr = h ? hi(r2) : lo(r2), ar = h ? hi(arg) : lo(arg);
-  if (KERNEL == PI_K_GAUSSIAN) return (rr < thr) ? __fmul_rn(ex2_approx(ar), a.w) : 0.f;
-  return (rr < thr) ? a.w : 0.f;
-}
-
 template <int KERNEL, int NT>
 __global__ void __launch_bounds__(NT) k_interact_fullload(FlParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -276,6 +276,7 @@ inline cudaError_t allow_max_smem(F *func) {
 
 cudaError_t launch_interact_global(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
+cudaError_t launch_interact_xpencil2(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 cudaError_t launch_interact_xpreg(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 // P: ordered pairs (i, j), j != i, r_ij < r_c, over the owned targets of the sorted state -> ctl->pairs

@@ -379,3 +379,22 @@ def test_run_host_after_submits():
     ctx.run_host_wait()
     for k in range(3):
         assert_parity(torch.stack(hout[k], 1).numpy(), wants[k], label=f"run {k}")
+
+
+@pytest.mark.parametrize("kernel", ["gaussian", "indicator", "candidate", "lj", "lowflop", "highflop"])
+def test_xpencil_interleaved_layout(kernel):
+    """The X-pencil's sub-cell-interleaved staging (tuning xpencil_layout = 1): configs[0] against
+    the oracle for every kernel, a clustered cloud with dense cells, and exact integer counts."""
+    c = synth.make_config("c0")
+    got, ctx = gpu_interact(c, "xpencil", kernel, tuning=dict(xpencil_layout=1))
+    want = oracle_interact(c, kernel)
+    assert_parity(got, want, label=f"interleaved {kernel}")
+    assert ctx.stats()["candidates"] == int(want["C"].sum())
+    if kernel in ("indicator", "candidate"):
+        c1 = synth.make_config("c0", qkind="ones")
+        got, _ = gpu_interact(c1, "xpencil", kernel, tuning=dict(xpencil_layout=1))
+        w = oracle_interact(c1, kernel)
+        assert np.array_equal(got[:, 0], w["P" if kernel == "indicator" else "C"].astype(np.float64))
+    cl = synth.clustered(1 << 14, synth.Grid(dims=(16, 16, 16), w=1 / 16), seed=240616094)
+    got, ctx = gpu_interact(cl, "xpencil", kernel, tuning=dict(xpencil_layout=1, xpencil_cap=200))
+    assert_parity(got, oracle_interact(cl, kernel), label=f"interleaved clustered {kernel}")

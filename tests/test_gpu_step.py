@@ -25,7 +25,9 @@ def state(ctx):
                                                   ("global", "lj", 4, None), ("xpreg", "gaussian", 2, None),
                                                   # every cell through the Par-Cell-SM pass
                                                   ("xpencil", "gaussian", 0, dict(xpencil_cap=16)),
-                                                  ("xpencil", "lj", 2, dict(xpencil_cap=16))])
+                                                  ("xpencil", "lj", 2, dict(xpencil_cap=16)),
+                                                  # the interleaved staging (records, not pairs)
+                                                  ("xpencil", "gaussian", 4, dict(xpencil_layout=1))])
 def test_step_matches_oracle(algo, kernel, xs, tune):
     """Three steps, each checked against the oracle at the GPU's pre-step state; the re-binning
     (counts carried by the update, R18 sub-cells) must be bit-exact per cell afterwards."""
