@@ -351,7 +351,7 @@ def strategies_at(a, dev, stream, name="c1"):
     x, y, z, q = (torch.from_numpy(v).to(dev) for v in (c.x, c.y, c.z, c.q))
     ctx.bin(x, y, z, q)
     out = {"workload": WORKLOADS.get(name, name), "unit": "candidate pair interactions/s"}
-    for algo in ("global", "fullload", "xpencil", "xpreg"):
+    for algo in ("global", "fullload", "xpencil", "xpreg", "half"):
         ctx.interact(algo, out=False)
         ms = []
         for _ in range(5):

@@ -110,8 +110,21 @@ typedef enum {
  *   PI_A_XPREG   : X-pencil-reg (§5.3): the targets
  *                  of a sub-box of cells in registers, the (By+2)(Bz+2) source X-pencils around
  *                  it staged one after the other, the box's own records copied to shared memory
- *                  from the registers.  Needs the sorted records (pi_bin / pi_step write them).  */
-typedef enum { PI_A_GLOBAL = 0, PI_A_FULLLOAD = 1, PI_A_XPENCIL = 2, PI_A_AUTO = 3, PI_A_XPREG = 4 } pi_algo;
+ *                  from the registers.  Needs the sorted records (pi_bin / pi_step write them).
+ *   PI_A_HALF    : Newton-3rd-law half-shell: every unordered pair
+ *                  evaluated once, by the target whose upper half-neighbourhood holds the
+ *                  source (4 of the 8 neighbour rows, the rest of its own row after it), and
+ *                  credited to both (phi_j gets q_i K, F_j = -F_i: Eq. (1));
+ *                  the source's share is a vector reduction into the sorted-order output.
+ *                  One thread per target as PI_A_GLOBAL; needs the sorted records.  */
+typedef enum {
+  PI_A_GLOBAL = 0,
+  PI_A_FULLLOAD = 1,
+  PI_A_XPENCIL = 2,
+  PI_A_AUTO = 3,
+  PI_A_XPREG = 4,
+  PI_A_HALF = 5
+} pi_algo;
 
 typedef struct {
   /* Global grid (PAPER.md:54-56 §2, :93 §3).  Cells are cubes of width cell_width; the box

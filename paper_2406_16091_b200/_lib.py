@@ -13,7 +13,7 @@ PI_OK, PI_EINVAL, PI_ECAPACITY, PI_EINAPPLICABLE, PI_ECUDA, PI_ENCCL, PI_ESTATE,
 STATUS_NAMES = ["PI_OK", "PI_EINVAL", "PI_ECAPACITY", "PI_EINAPPLICABLE", "PI_ECUDA", "PI_ENCCL", "PI_ESTATE",
                 "PI_EDEVICE"]
 KERNELS = {"gaussian": 0, "indicator": 1, "candidate": 2, "lj": 3, "lowflop": 4, "highflop": 5}
-ALGOS = {"global": 0, "fullload": 1, "xpencil": 2, "auto": 3, "xpreg": 4}
+ALGOS = {"global": 0, "fullload": 1, "xpencil": 2, "auto": 3, "xpreg": 4, "half": 5}
 
 
 class pi_config(ctypes.Structure):

@@ -567,6 +567,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
       break;
     case PI_A_FULLLOAD: e = launch_interact_fullload(c->g, c->kp, a, c->stream); break;
     case PI_A_XPREG: e = launch_interact_xpreg(c->g, c->kp, a, c->stream); break;
+    case PI_A_HALF: e = launch_interact_half(c->g, c->kp, a, c->stream); break;
     default: return fail(c, PI_EINVAL, "unknown algo %d", (int)algo);
   }
   phase_end(c, 1);

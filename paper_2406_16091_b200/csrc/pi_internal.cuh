@@ -281,5 +281,6 @@ cudaError_t launch_interact_fullload(const Geom &g, const KParams &k, const Inte
 cudaError_t launch_interact_xpreg(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 // P: ordered pairs (i, j), j != i, r_ij < r_c, over the owned targets of the sorted state -> ctl->pairs
 cudaError_t launch_count_pairs(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
+cudaError_t launch_interact_half(const Geom &g, const KParams &k, const InteractArgs &a, cudaStream_t s);
 
 }  // namespace pi

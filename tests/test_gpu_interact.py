@@ -12,7 +12,7 @@ from oracle import reference as ref
 from tests._util import assert_parity, ctx_for, gpu_interact, oracle_interact, to_dev
 
 pytestmark = pytest.mark.gpu
-ALGOS = ["global", "xpencil", "fullload", "xpreg"]
+ALGOS = ["global", "xpencil", "fullload", "xpreg", "half"]
 # Every strategy computes r^2 from differences of the raw fp32 positions: for dyadic inputs
 # every step is exact, so pairs at exactly r = r_c are excluded exactly (band 0) by all of them.
 
@@ -300,7 +300,7 @@ def oracle_candidates(c):
     return int((n3 * nb).sum() - c.n)
 
 
-@pytest.mark.parametrize("algo", ["global", "fullload", "xpreg"])
+@pytest.mark.parametrize("algo", ["global", "fullload", "xpreg", "half"])
 def test_full_size_other_strategies(algo):
     """The global baseline and the full load at full size: configs[2] ppc 8 (2^24 on 128^3),
     sampled targets against the oracle, candidates against the oracle's closed form."""

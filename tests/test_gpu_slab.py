@@ -50,7 +50,7 @@ def _dev(a):
 
 
 @pytest.mark.parametrize("P", [2, 4])
-@pytest.mark.parametrize("algo", ["global", "xpencil", "fullload", "xpreg"])
+@pytest.mark.parametrize("algo", ["global", "xpencil", "fullload", "xpreg", "half"])
 def test_slab_bin_interact_matches_whole_cloud(P, algo):
     c = synth.make_config("c0", n=4 * 4096)
     g = c.grid
@@ -112,7 +112,7 @@ def test_slab_binning_counts_exact():
         assert offsets[-1] == counts.sum()
 
 
-@pytest.mark.parametrize("algo", ["xpencil", "global"])
+@pytest.mark.parametrize("algo", ["xpencil", "global", "half"])
 def test_slab_steps_migrate_and_match_oracle(algo):
     c = synth.make_config("c0", n=4 * 4096)
     g = c.grid

@@ -23,6 +23,7 @@ def state(ctx):
                                                   ("fullload", "gaussian", 0, None), ("xpencil", "gaussian", 1, None),
                                                   ("xpencil", "gaussian", 8, None), ("xpencil", "lj", 0, None),
                                                   ("global", "lj", 4, None), ("xpreg", "gaussian", 2, None),
+                                                  ("half", "gaussian", 0, None), ("half", "lj", 2, None),
                                                   # every cell through the Par-Cell-SM pass
                                                   ("xpencil", "gaussian", 0, dict(xpencil_cap=16)),
                                                   ("xpencil", "lj", 2, dict(xpencil_cap=16)),
