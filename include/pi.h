@@ -171,8 +171,11 @@ typedef struct {
   int64_t exchange_bytes;    /* a8: payload bytes this rank sent to its neighbours so far      */
   double phase_ms[4];        /* device time of the last bin (a1-a4), interaction (a5-a7),
                                 exchange (a8) and host-path copies, from CUDA events recorded
-                                on the context stream around each phase                      */
-  int64_t reserved[3];
+                                on the context stream around each phase (the overlapped
+                                exchange: on the library's exchange stream)                   */
+  int64_t overlapped_steps;  /* a8: pi_step calls whose exchange ran beside the interior
+                                interaction (pi_tuning.exchange_overlap)                      */
+  int64_t reserved[2];
 } pi_stats;
 
 /* Tuning knobs of the launch configuration (a5).  Zero fields mean "library default".   */
@@ -190,7 +193,9 @@ typedef struct {
   int32_t xpencil_slots;     /* X-pencil: staging slots per block (2..4; default 2)         */
   int32_t xpencil_targets;   /* X-pencil: targets per consumer lane, 1 or 2 (default 1; 2
                                 reads each staged source once for two consecutive targets;
-                                the CANDIDATE test kernel always walks one)                 */
+                                the CANDIDATE test kernel always walks one); 3 = cell groups:
+                                a warp per target cell, 32 / n lanes per target over the
+                                union window of the cell (measured slower)     */
   int32_t exchange_full;     /* a8 (nranks > 1): 0 (default) = two-phase exchange, the counts
                                 first, then exactly the counted records (one stream
                                 synchronisation per exchange); 1 = the whole fixed-capacity
@@ -199,7 +204,12 @@ typedef struct {
                                 runs per target; xpencil_targets applies); 1 = X-sub-cell-
                                 interleaved (a target's candidates are one contiguous range,
                                 one thread per target pair; measured slower)     */
-  int32_t reserved[4];
+  int32_t exchange_overlap;  /* a8 (nranks > 1, X-pencil, >= 4 owned X layers): 0 (default) =
+                                the step computes the first and last 2 owned layers first, then
+                                the interior while a second (library-created) stream exchanges
+                                the migrants and the next step's ghosts; 1 = serial exchange at
+                                the start of the next step                                    */
+  int32_t reserved[3];
 } pi_tuning;
 
 PI_API int32_t pi_abi_version(void);
@@ -251,7 +261,12 @@ PI_API pi_status pi_interact(pi_ctx ctx, pi_algo algo, float *phi, float *fx, fl
  * walls (reading of PAPER.md:65), in sorted order.  Collective when
  * nranks > 1: before re-binning, owned particles whose updated global X cell left the slab
  * migrate to rank -1 / +1 (at most one slab per step, else flag 4), then the ghost layers
- * are exchanged again.  The first call after pi_bin reuses that binning.                   */
+ * are exchanged again.  The first call after pi_bin reuses that binning.  With the X-pencil
+ * and >= 4 owned X layers (pi_tuning.exchange_overlap = 0) the exchange is overlapped: the
+ * step computes the first and last 2 owned layers first, then the interior while the
+ * migrants and the next step's ghosts are exchanged on a second stream; the call returns
+ * with the context stream ordered after that exchange.  The overlap needs |dt F| < w per
+ * step (else flag 4, as for migration beyond one slab).                                     */
 PI_API pi_status pi_step(pi_ctx ctx, pi_algo algo, float dt);
 
 /* End-to-end call on HOST buffers: copies x,y,z,q (n floats each) host->device, bins,

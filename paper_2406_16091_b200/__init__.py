@@ -141,13 +141,14 @@ class Context:
             pass
 
     def set_tuning(self, xpencil_len=0, xpencil_cap=0, fullload_box=(0, 0, 0), fullload_cap=0, threads=0,
-                   xpencil_slots=0, xpencil_targets=0, exchange_full=0, xpencil_layout=0):
+                   xpencil_slots=0, xpencil_targets=0, exchange_full=0, xpencil_layout=0, exchange_overlap=0):
         t = L.pi_tuning()
         t.xpencil_len, t.xpencil_cap, t.fullload_cap, t.threads = xpencil_len, xpencil_cap, fullload_cap, threads
         t.xpencil_slots = xpencil_slots
         t.xpencil_targets = xpencil_targets
         t.exchange_full = exchange_full
         t.xpencil_layout = xpencil_layout
+        t.exchange_overlap = exchange_overlap
         for a in range(3):
             t.fullload_box[a] = int(fullload_box[a])
         self._check(self._lib.pi_set_tuning(self._h, ctypes.byref(t)))

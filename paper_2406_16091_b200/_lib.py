@@ -28,14 +28,16 @@ class pi_stats(ctypes.Structure):
     _fields_ = [("n_owned", ctypes.c_int64), ("n_ghost", ctypes.c_int64), ("max_per_cell", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("candidates", ctypes.c_int64), ("fallback_cells", ctypes.c_int64),
                 ("migrants_in", ctypes.c_int64), ("migrants_out", ctypes.c_int64), ("steps", ctypes.c_int64),
-                ("exchange_bytes", ctypes.c_int64), ("phase_ms", ctypes.c_double * 4), ("reserved", ctypes.c_int64 * 3)]
+                ("exchange_bytes", ctypes.c_int64), ("phase_ms", ctypes.c_double * 4),
+                ("overlapped_steps", ctypes.c_int64), ("reserved", ctypes.c_int64 * 2)]
 
 
 class pi_tuning(ctypes.Structure):
     _fields_ = [("xpencil_len", ctypes.c_int32), ("xpencil_cap", ctypes.c_int32),
                 ("fullload_box", ctypes.c_int32 * 3), ("fullload_cap", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("xpencil_slots", ctypes.c_int32), ("xpencil_targets", ctypes.c_int32),
-                ("exchange_full", ctypes.c_int32), ("xpencil_layout", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("exchange_full", ctypes.c_int32), ("xpencil_layout", ctypes.c_int32),
+                ("exchange_overlap", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 P = ctypes.c_void_p

@@ -38,9 +38,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    hdr = max(os.path.getmtime(h) for h in deps() if not h.endswith(".cu"))
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr, os.path.getmtime(src)):
+            continue  # up to date (a failed compile leaves no newer object)
         cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-dc" if False else "-c", src, "-o", obj]
         log = open(obj + ".log", "w")
         procs.append((subprocess.Popen(cmd, stdout=log, stderr=subprocess.STDOUT), cmd, obj))

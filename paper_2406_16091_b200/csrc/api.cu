@@ -21,7 +21,7 @@ size_t align_up(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
   size_t ctl, counts, offsets, foffsets, pcounts, ptsum, dense, tiles, bcur, rec, sid, perm, urec, uid, tidx, outs, io, pairs;
-  size_t xrec, xid, xperm, msg[4];  // nranks > 1
+  size_t xrec, xid, xperm, msg[8];  // nranks > 1 (two message sets)
   size_t total;
 };
 
@@ -91,7 +91,7 @@ Layout make_layout(const pi_config *cfg) {
     L.xrec = take(sizeof(float4) * (size_t)cap);
     L.xid = take(sizeof(int32_t) * (size_t)cap);
     L.xperm = take(sizeof(int32_t) * (size_t)cap);
-    for (int k = 0; k < 4; ++k) L.msg[k] = take(msg_bytes(sg.cap_msg));
+    for (int k = 0; k < 8; ++k) L.msg[k] = take(msg_bytes(sg.cap_msg));
   }
   L.total = o;
   return L;
@@ -177,6 +177,11 @@ struct pi_ctx_s {
   cudaStream_t h2d, d2h;
   cudaEvent_t ev_sub, ev_in[RH_SETS], ev_binned[RH_SETS], ev_out[RH_SETS], ev_done[RH_SETS];
   long long rh_issued, rh_done;
+  // a8 overlapped step (nranks > 1): exchange stream and its events
+  cudaStream_t xs;
+  cudaEvent_t ev_bnd, ev_xdone;
+  bool ovl_ready;    // the migrant and ghost messages of the pending re-binning have been exchanged
+  long long ovl_steps;
   char err[512];
 };
 
@@ -364,6 +369,7 @@ pi_status pi_create(const pi_config *cfg, void *workspace, size_t ws_bytes, pi_c
     S.sendR = c->ws + lay.msg[1];
     S.recvL = c->ws + lay.msg[2];
     S.recvR = c->ws + lay.msg[3];
+    S.g = MsgSet{c->ws + lay.msg[4], c->ws + lay.msg[5], c->ws + lay.msg[6], c->ws + lay.msg[7]};
     S.xrec = reinterpret_cast<float4 *>(c->ws + lay.xrec);
     S.xid = reinterpret_cast<int32_t *>(c->ws + lay.xid);
     S.xperm = reinterpret_cast<int32_t *>(c->ws + lay.xperm);
@@ -404,6 +410,11 @@ pi_status pi_destroy(pi_ctx c) {
       }
       cudaStreamDestroy(c->h2d);
       cudaStreamDestroy(c->d2h);
+    }
+    if (c->xs) {
+      cudaEventDestroy(c->ev_bnd);
+      cudaEventDestroy(c->ev_xdone);
+      cudaStreamDestroy(c->xs);
     }
     delete c->slab.tr;
     if (c->slab.hcnt) cudaFreeHost(c->slab.hcnt);
@@ -503,6 +514,7 @@ pi_status pi_bin(pi_ctx c, int64_t n, const float *x, const float *y, const floa
   c->n = n;
   c->state = 1;
   c->need_bin = false;
+  c->ovl_ready = false;
   c->interacted = false;
   return PI_OK;
 }
@@ -516,8 +528,11 @@ static pi_algo resolve_auto(pi_ctx c, pi_algo algo) {
   return ppc < 3.0 ? PI_A_GLOBAL : PI_A_XPENCIL;
 }
 
+// xr (X-pencil only): the target X layers [xr0, xr1) + [xr2, xr3) of this launch (NULL: all
+// owned); part: 0 the whole interaction, 1 / 2 its first / second launch (statistics reset by
+// the first, phase timing over both), reserve: SMs left to kernels running beside it
 static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, float *fy, float *fz, bool integrate,
-                             float dt) {
+                             float dt, const int *xr = nullptr, int part = 0, int reserve = 0) {
   algo = resolve_auto(c, algo);
   InteractArgs a{};
   const bool multi = c->cfg.nranks > 1;
@@ -554,11 +569,20 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
   a.dense = c->dense;
   a.fb[0] = c->tune.fullload_box[0]; a.fb[1] = c->tune.fullload_box[1]; a.fb[2] = c->tune.fullload_box[2];
   a.fb_cap = c->tune.fullload_cap;
-  cudaError_t e = cudaMemsetAsync(&c->ctl->fallback_cells, 0,
-                                  sizeof(DevCtl) - offsetof(DevCtl, fallback_cells), c->stream);
+  if (xr) {
+    a.xr_set = true;
+    for (int k = 0; k < 4; ++k) a.xr[k] = xr[k];
+  }
+  a.reserve_sms = reserve;
+  cudaError_t e = part == 2
+                      // the second launch: a fresh item counter and dense-cell tickets (the first
+                      // launch's listed cells are all computed: every entry is free again)
+                      ? cudaMemsetAsync(&c->ctl->xp_items, 0, sizeof(unsigned long long) * 5, c->stream)
+                      : cudaMemsetAsync(&c->ctl->fallback_cells, 0,
+                                        sizeof(DevCtl) - offsetof(DevCtl, fallback_cells), c->stream);
   if (e != cudaSuccess) return cuda_check(c, e, "pi_interact memset");
   if (algo == PI_A_AUTO) algo = PI_A_XPENCIL;
-  phase_begin(c, 1);
+  if (part != 2) phase_begin(c, 1);
   switch (algo) {
     case PI_A_GLOBAL: e = launch_interact_global(c->g, c->kp, a, c->stream); break;
     case PI_A_XPENCIL:
@@ -570,7 +594,7 @@ static pi_status do_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, floa
     case PI_A_HALF: e = launch_interact_half(c->g, c->kp, a, c->stream); break;
     default: return fail(c, PI_EINVAL, "unknown algo %d", (int)algo);
   }
-  phase_end(c, 1);
+  if (part != 1) phase_end(c, 1);
   if (e == cudaErrorNotSupported) return fail(c, PI_EINAPPLICABLE, "strategy not applicable to this grid");
   return cuda_check(c, e, "pi_interact");
 }
@@ -586,12 +610,80 @@ pi_status pi_interact(pi_ctx c, pi_algo algo, float *phi, float *fx, float *fy, 
   return s;
 }
 
+// a8 with the exchange overlapped: the X-pencil first computes (and updates)
+// the first and last 2 owned X layers -- every particle that can leave the slab or end up in a
+// boundary layer (a ghost of the next step) is there, |dt F| < w (reading C11) -- then the
+// interior layers, while a second stream sorts the boundary particles into migrant and ghost
+// messages, exchanges the migrants, adds the arrivals to the ghosts and exchanges those.  The
+// next pi_step only compacts the stayers and appends what arrived.
+static bool overlap_ok(pi_ctx c, pi_algo algo) {
+  return c->cfg.nranks > 1 && algo == PI_A_XPENCIL && c->tune.xpencil_layout != 1 && c->tune.exchange_overlap == 0 &&
+         c->slab.Lx >= 4;
+}
+
+static pi_status step_overlapped(pi_ctx c, float dt) {
+  SlabState &S = c->slab;
+  const long long cap = c->cfg.capacity;
+  cudaError_t e = cudaSuccess;
+  if (!c->xs) {
+    e = cudaStreamCreateWithFlags(&c->xs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_bnd, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_xdone, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_check(c, e, "exchange stream");
+  }
+  const int lo = c->g.own_lo, hi = c->g.own_hi;
+  const int bnd[4] = {lo, lo + 2, hi - 2, hi}, mid[4] = {lo + 2, hi - 2, 0, 0};
+  const bool interior = hi - 2 > lo + 2;
+  pi_status st = do_interact(c, PI_A_XPENCIL, nullptr, nullptr, nullptr, nullptr, true, dt, bnd, interior ? 1 : 0);
+  if (st != PI_OK) return st;
+  if ((e = cudaEventRecord(c->ev_bnd, c->stream)) != cudaSuccess) return cuda_check(c, e, "event");
+  if ((e = cudaStreamWaitEvent(c->xs, c->ev_bnd, 0)) != cudaSuccess) return cuda_check(c, e, "event wait");
+  cudaEventRecord(c->ev[2][0], c->xs);
+  c->ev_used[2] = true;
+  if ((e = slab_reset(S, c->ctl, c->xs, 0, false)) != cudaSuccess) return cuda_check(c, e, "slab reset");
+  if ((e = slab_reset(S, c->ctl, c->xs, 1, false)) != cudaSuccess) return cuda_check(c, e, "slab reset");
+  if ((e = slab_migrate_boundary(S, c->g, cap, c->rec, c->urec, c->uid, c->ctl, c->xs)) != cudaSuccess)
+    return cuda_check(c, e, "boundary migrate");
+  // the interior launch is queued before the exchange blocks this thread on the host; two SMs
+  // stay free for the transport's and the exchange kernels
+  if (interior) {
+    st = do_interact(c, PI_A_XPENCIL, nullptr, nullptr, nullptr, nullptr, true, dt, mid, 2, 2);
+    if (st != PI_OK) return st;
+  }
+  if ((e = slab_exchange(S, c->xs, 0)) != cudaSuccess) return fail(c, PI_ENCCL, "migration exchange failed");
+  if ((e = slab_ghost_arrivals(S, c->g, c->ctl, c->xs)) != cudaSuccess) return cuda_check(c, e, "ghost arrivals");
+  if ((e = slab_exchange(S, c->xs, 1)) != cudaSuccess) return fail(c, PI_ENCCL, "ghost exchange failed");
+  cudaEventRecord(c->ev[2][1], c->xs);
+  if ((e = cudaEventRecord(c->ev_xdone, c->xs)) != cudaSuccess) return cuda_check(c, e, "event");
+  if ((e = cudaStreamWaitEvent(c->stream, c->ev_xdone, 0)) != cudaSuccess) return cuda_check(c, e, "event wait");
+  c->ovl_ready = true;
+  c->ovl_steps++;
+  return PI_OK;
+}
+
 pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
   if (!c) return PI_EINVAL;
   algo = resolve_auto(c, algo);
   if (c->state == 0) return fail(c, PI_ESTATE, "pi_step before pi_bin");
   if (!std::isfinite(dt)) return fail(c, PI_EINVAL, "dt must be finite");
-  if (c->need_bin) {
+  if (c->need_bin && c->ovl_ready) {
+    // the previous (overlapped) step exchanged the migrants and ghosts already: compact the
+    // stayers, append the arrivals (set 0) and the ghosts (set 1), bin
+    SlabState &S = c->slab;
+    const long long cap = c->cfg.capacity;
+    cudaError_t e = cudaMemsetAsync(&c->ctl->n_stay, 0, sizeof(long long), c->stream);
+    if (e == cudaSuccess) e = slab_migrate(S, c->g, cap, c->rec, c->urec, c->uid, c->ctl, c->stream, false);
+    if (e == cudaSuccess)
+      e = slab_append(S, &c->ctl->n_stay, &c->ctl->n_owned, &c->ctl->migrants_in, &c->ctl->migrants_out, cap, c->ctl,
+                      c->stream, 0);
+    if (e == cudaSuccess)
+      e = slab_append(S, &c->ctl->n_owned, &c->ctl->n_total, &c->ctl->ghosts_in, &c->ctl->pad2[1], cap, c->ctl,
+                      c->stream, 1);
+    if (e != cudaSuccess) return cuda_check(c, e, "overlapped re-binning");
+    c->ovl_ready = false;
+    pi_status s = do_bin(c, cap, nullptr, nullptr, nullptr, nullptr, S.xid, S.xrec, S.xperm, &c->ctl->n_total);
+    if (s != PI_OK) return s;
+  } else if (c->need_bin) {
     pi_status s;
     if (c->cfg.nranks > 1) {
       // a8: migration of the particles whose updated cell left the slab, then ghosts + bin
@@ -616,7 +708,8 @@ pi_status pi_step(pi_ctx c, pi_algo algo, float dt) {
     }
     if (s != PI_OK) return s;
   }
-  pi_status s = do_interact(c, algo, nullptr, nullptr, nullptr, nullptr, true, dt);
+  pi_status s = overlap_ok(c, algo) ? step_overlapped(c, dt)
+                                     : do_interact(c, algo, nullptr, nullptr, nullptr, nullptr, true, dt);
   if (s != PI_OK) return s;
   c->state = 2;
   c->need_bin = true;
@@ -808,6 +901,7 @@ pi_status pi_get_stats(pi_ctx c, pi_stats *out) {
   out->candidates = (int64_t)cand;
   out->fallback_cells = (int64_t)h.fallback_cells;
   out->steps = c->steps;
+  out->overlapped_steps = c->ovl_steps;
   out->exchange_bytes = c->slab.bytes_sent;
   for (int k = 0; k < 4; ++k) {
     float ms = 0.f;

@@ -44,6 +44,7 @@ namespace {
 
 constexpr int MAX_SLOTS = 4;
 constexpr int META = 16;
+constexpr size_t WT_BYTES = 20 * 32 * 4;
 constexpr float DUMMY_X = 1.0e30f;  // inert partner of an odd run's last record: K = 0, q = 0
 
 struct XpParams {
@@ -63,8 +64,11 @@ struct XpParams {
   int nslot;         // staging slots (2..MAX_SLOTS)
   int tpl;           // targets per consumer lane (1 or 2)
   int32_t *dense;    // cells whose window alone does not fit a slot: listed for Par-Cell-SM
-  int nseg;          // segments per X row
+  int nseg;          // segments per X row (nseg0 of them in the first X range)
+  int nseg0;
+  int xr[4];         // target X layers (local): [xr0, xr1) then [xr2, xr3) (may be empty)
   long long nitems;  // rows x segments
+  int reserve;       // SMs left free (the exchange kernels overlapping this launch)
 };
 
 // Slot: SA[capp] | SB[capp] float4 (source pairs, planes A and B) | meta[16] | O[9][LF] | rb[32],
@@ -81,7 +85,8 @@ __host__ __device__ inline size_t slot_bytes(int L, int capp, int sx) {
   return (size_t)capp * 32 + (size_t)slot_words(L, sx) * 4;
 }
 __host__ __device__ inline size_t xp_smem_bytes(int L, int capp, int sx, int nslot) {
-  return 128 + nslot * slot_bytes(L, capp, sx) + (size_t)9 * lf_of(L, sx) * 4;  // + offsets staging
+  // + offsets staging + the cell-group consumers' run tables (32 ints per warp, <= 20 warps)
+  return 128 + nslot * slot_bytes(L, capp, sx) + (size_t)9 * lf_of(L, sx) * 4 + WT_BYTES;
 }
 
 struct Slot {
@@ -128,8 +133,9 @@ __device__ __forceinline__ void item_geom(const XpParams &p, long long item, int
   const long long row = item / p.nseg;
   cy = (int)(row % p.g.ny);
   cz = (int)(row / p.g.ny);
-  x0 = p.g.own_lo + seg * p.L;
-  Lseg = min(p.L, p.g.own_hi - x0);
+  const bool first = seg < p.nseg0;
+  x0 = first ? p.xr[0] + seg * p.L : p.xr[2] + (seg - p.nseg0) * p.L;
+  Lseg = min(p.L, (first ? p.xr[1] : p.xr[3]) - x0);
 }
 __device__ __forceinline__ void cp_async4(int *dst, const int *src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 4 : 0)
@@ -292,7 +298,58 @@ __device__ __forceinline__ void walk9x2(const Slot &sl, int LF, int sx, int ja, 
                    lo(fz1) + hi(fz1) - s1.w);
 }
 
-// UPD: pi_step (update + carried counts in the epilogue); TPL: targets per lane (1: walk9, 2: walk9x2)
+// Cell-group walk (TPL = 0): the targets of ONE cell share a warp, k = 32 / n_t lanes per
+// target, and every target walks the union window of the cell's targets (the fine X window of
+// each target, reduced min / max over the warp: a source of the union outside a target's own
+// window has |dx| >= r_c, so it adds exactly 0 for the cutoff kernels, as in walk9x2).  The 9
+// runs of that window are one flattened sequence of Np staged pairs (wt: cumulative ends
+// wt[0..8], staged pair of sequence index g = wt[16 + r] + g), and the k lanes of a target take
+// the indices g = jj, jj + k, ...: no per-run tails, and the lanes of all targets read the same
+// k staged pairs at a time (k distinct shared-memory addresses per LDS.128 instead of up to 32).
+// Returns the lane's partial sums (the self pair is in exactly one lane's share).
+template <int KERNEL>
+__device__ __forceinline__ float4 walk_flat(const Slot &sl, const int *wt, int Np, int g, int k, const float4 me,
+                                            const float thr, const float mc2, const KParams &kp) {
+  const float4 *__restrict__ S = sl.S;
+  const float4 *__restrict__ SB = sl.SB;
+  p2 phi = pk(0.f), fx = pk(0.f), fy = pk(0.f), fz = pk(0.f);
+  p2 phb = pk(0.f), fxb = pk(0.f), fyb = pk(0.f), fzb = pk(0.f);
+  int r = 0, end = wt[0], off = wt[16];
+  for (; g + k < Np; g += 2 * k) {
+    while (g >= end) {
+      ++r;
+      end = wt[r];
+      off = wt[16 + r];
+    }
+    const int pa = off + g;
+    const int g2 = g + k;
+    while (g2 >= end) {
+      ++r;
+      end = wt[r];
+      off = wt[16 + r];
+    }
+    const int pb = off + g2;
+    const SrcPair s0 = load_pair(S, SB, pa), s1 = load_pair(S, SB, pb);
+    src_eval<KERNEL>(s0, me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
+    src_eval<KERNEL>(s1, me.x, me.y, me.z, thr, mc2, phb, fxb, fyb, fzb, &kp);
+  }
+  if (g < Np) {
+    while (g >= end) {
+      ++r;
+      end = wt[r];
+      off = wt[16 + r];
+    }
+    src_eval<KERNEL>(load_pair(S, SB, off + g), me.x, me.y, me.z, thr, mc2, phi, fx, fy, fz, &kp);
+  }
+  phi = add2(phi, phb);
+  fx = add2(fx, fxb);
+  fy = add2(fy, fyb);
+  fz = add2(fz, fzb);
+  return make_float4(lo(phi) + hi(phi), lo(fx) + hi(fx), lo(fy) + hi(fy), lo(fz) + hi(fz));
+}
+
+// UPD: pi_step (update + carried counts in the epilogue); TPL: targets per lane (1: walk9,
+// 2: walk9x2), 0: cell groups (walk_flat)
 template <int KERNEL, int NC, bool UPD, int TPL>
 __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -419,7 +476,10 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     }
   } else {
     // ================================ consumers ================================
-    const float thr = p.kp.rc2, mc2 = -p.kp.c2;
+    // in vector registers (a shuffle cannot be rematerialised): read from the constant bank,
+    // ptxas reloaded them into uniform registers in every iteration of the walk (3 LDCU + MOV
+    // of 47 instructions per 2 source pairs)
+    const float thr = __shfl_sync(0xffffffffu, p.kp.rc2, 0), mc2 = __shfl_sync(0xffffffffu, -p.kp.c2, 0);
     for (unsigned use = 0;; ++use) {
       const int s = use % NSLOT;
       const Slot sl = slot_at(slots, L, p.capp, sx, s);
@@ -469,6 +529,74 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
           write_output<UPD>(p.out, g, gs, me, r.x, 0.f, 0.f, 0.f, fold);
         }
       };
+      if (TPL == 0) {
+        // cell groups: a batch is one target cell j of the round (in chunks of <= 32 targets)
+        int *wt = reinterpret_cast<int *>(slots + (size_t)NSLOT * slot_bytes(L, p.capp, sx) +
+                                          (size_t)9 * LF * 4) + warp * 32;
+        for (;;) {
+          int b = 0;
+          if (lane == 0) b = atomicAdd(&sl.meta[6], 1);
+          b = __shfl_sync(0xffffffffu, b, 0);
+          const int j = ja + b;
+          if (j > jb) break;
+          const int cs = O4[j * sx], na = O4[(j + 1) * sx] - cs;
+          for (int c0 = 0; c0 < na; c0 += 32) {
+            const int nt = min(32, na - c0);
+            const float rn = __frcp_rn((float)nt);
+            const int k = (int)(32.5f * rn);               // floor(32 / nt)
+            const int jj = (int)(((float)lane + 0.5f) * rn);  // floor(lane / nt)
+            const int t = lane - jj * nt;
+            const int gs = cs + c0 + t;
+            int jt, sub, klo, khi;
+            float4 me;
+            setup(gs, jt, sub, me, klo, khi);
+            klo = __reduce_min_sync(0xffffffffu, klo);
+            khi = __reduce_max_sync(0xffffffffu, khi);
+            // the union window's 9 runs as one sequence of staged pairs
+            int np = 0, p0 = 0;
+            if (lane < 9) {
+              const int a = sl.O[lane * LF + klo], e = sl.O[lane * LF + khi + 1];
+              if (e > a) {
+                p0 = sl.rb[16 + lane] + (a >> 1);
+                np = sl.rb[16 + lane] + ((e - 1) >> 1) - p0 + 1;
+              }
+            }
+            int incl = np;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+              const int v = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += v;
+            }
+            const int Np = __shfl_sync(0xffffffffu, incl, 8);
+            if (lane < 9) {
+              wt[lane] = incl;
+              wt[16 + lane] = p0 - (incl - np);
+            }
+            __syncwarp();
+            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (jj < k) r = walk_flat<KERNEL>(sl, wt, Np, jj, k, me, thr, mc2, p.kp);
+            // the k partial sums of each target (lanes t, t + nt, ...), tree over jj
+            for (int m = 1; m < k; m <<= 1) {
+              const float ox = __shfl_down_sync(0xffffffffu, r.x, m * nt);
+              const float oy = __shfl_down_sync(0xffffffffu, r.y, m * nt);
+              const float oz = __shfl_down_sync(0xffffffffu, r.z, m * nt);
+              const float ow = __shfl_down_sync(0xffffffffu, r.w, m * nt);
+              if ((jj & (2 * m - 1)) == 0 && jj + m < k) {
+                r.x += ox;
+                r.y += oy;
+                r.z += oz;
+                r.w += ow;
+              }
+            }
+            if (jj == 0) {
+              const float4 st = self_terms<KERNEL>(me, p.kp);  // the self pair's exact term
+              r = make_float4(r.x - st.x, r.y - st.y, r.z - st.z, r.w - st.w);
+              finish(gs, jt, sub, me, r);
+            }
+            __syncwarp();  // wt is rewritten by the next chunk
+          }
+        }
+      } else
       for (;;) {
         int b = 0;
         if (lane == 0) b = atomicAdd(&sl.meta[6], 32 * TPL);
@@ -548,7 +676,7 @@ cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (NC + 1) * 32, smem);
     if (occ < 1) occ = 1;
-    long long blocks = (long long)sms * occ;
+    long long blocks = (long long)sms * occ - p.reserve;
     if (blocks > p.nitems) blocks = p.nitems;
     if (blocks < 1) blocks = 1;
     kern<<<(int)blocks, (NC + 1) * 32, smem, s>>>(p);
@@ -558,6 +686,17 @@ cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
   // two targets per lane for the cutoff kernels (walk9x2 relies on exact exclusion outside a
   // target's own window); the CANDIDATE test kernel and masked grids walk one target per lane
   const bool two = p.tpl == 2 && !p.mask;
+  const bool grp = p.tpl == 0 && !p.mask;  // cell groups (walk_flat): the cutoff kernels
+  if (grp) {
+    switch (p.kp.kernel) {
+      case PI_K_GAUSSIAN: return upd ? go(k_interact_xpencil<PI_K_GAUSSIAN, NC, true, 0>) : go(k_interact_xpencil<PI_K_GAUSSIAN, NC, false, 0>);
+      case PI_K_INDICATOR: return upd ? go(k_interact_xpencil<PI_K_INDICATOR, NC, true, 0>) : go(k_interact_xpencil<PI_K_INDICATOR, NC, false, 0>);
+      case PI_K_LJ: return upd ? go(k_interact_xpencil<PI_K_LJ, NC, true, 0>) : go(k_interact_xpencil<PI_K_LJ, NC, false, 0>);
+      case PI_K_LOWFLOP: return upd ? go(k_interact_xpencil<PI_K_LOWFLOP, NC, true, 0>) : go(k_interact_xpencil<PI_K_LOWFLOP, NC, false, 0>);
+      case PI_K_HIGHFLOP: return upd ? go(k_interact_xpencil<PI_K_HIGHFLOP, NC, true, 0>) : go(k_interact_xpencil<PI_K_HIGHFLOP, NC, false, 0>);
+      default: break;  // CANDIDATE: one target per lane (masked ends)
+    }
+  }
   switch (p.kp.kernel) {
     case PI_K_GAUSSIAN:
       if (two) return upd ? go(k_interact_xpencil<PI_K_GAUSSIAN, NC, true, 2>) : go(k_interact_xpencil<PI_K_GAUSSIAN, NC, false, 2>);
@@ -623,7 +762,20 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   p.kp = k;
   p.out = a.out;
   p.ctl = a.ctl;
-  const int own = g.own_hi - g.own_lo;
+  // the target X layers: the owned ones, or the caller's ranges (a8 overlap: the slab's boundary
+  // layers first, then the interior while the exchange runs)
+  int xr[4] = {g.own_lo, g.own_hi, 0, 0};
+  if (a.xr_set)
+    for (int k = 0; k < 4; ++k) xr[k] = a.xr[k];
+  const int own = max(xr[1] - xr[0], xr[3] - xr[2]);
+  if (own <= 0) return cudaSuccess;
+  for (int k = 0; k < 4; ++k) p.xr[k] = xr[k];
+  p.reserve = a.reserve_sms;
+  auto segs = [&]() {
+    p.nseg0 = (xr[1] - xr[0] + p.L - 1) / p.L;
+    p.nseg = p.nseg0 + (xr[3] - xr[2] + p.L - 1) / p.L;
+    p.nitems = (long long)p.nseg * g.ny * g.nz;
+  };
   // segment length: ~512 targets per item at the mean density (64 cells at 8 per cell, up to
   // 256 at 2 or fewer), so a slot feeds the consumer warps at low densities too (configs[2]
   // ppc 1: 7.0 -> 3.8 ms with 256 instead of 64; ppc 4: 2.43 -> 1.88 ms with 128)
@@ -632,27 +784,27 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   p.L = a.tx_len > 0 ? a.tx_len : l_auto;
   if (p.L > 512) p.L = 512;
   if (p.L > own) p.L = own;
-  p.nseg = (own + p.L - 1) / p.L;
-  p.nitems = (long long)p.nseg * g.ny * g.nz;
+  segs();
   p.foffsets = a.foffsets;
   p.sx = g.sx;
   p.mask = k.kernel == PI_K_CANDIDATE || g.nx < 4;
   const int nc = a.threads > 0 ? a.threads / 32 : 20;
   p.nslot = a.slots >= 2 ? min(a.slots, MAX_SLOTS) : 2;
   p.dense = a.dense;
-  p.tpl = a.tpl == 2 ? 2 : 1;  // default 1: two per lane measured slower
+  // targets per lane: 1 (one per lane), 2 (two per lane, measured slower), 0 (cell
+  // groups, walk_flat; tuning value 3)
+  p.tpl = a.tpl == 2 ? 2 : (a.tpl == 3 ? 0 : 1);
   const size_t max_smem = 227 * 1024;
   // the segment must leave room for slots of a useful size: the fixed tables (offsets per X
   // sub-cell boundary of every slot and of the prefetch stage) grow with L * sx (ADVICE r01:
   // L = 256 with sx = 16 did not fit at all).  Halve L until two slots hold the windows of a
   // few cells at the mean density.
   auto fixed_of = [&](int L) {
-    return 128 + (size_t)9 * lf_of(L, p.sx) * 4 + (size_t)p.nslot * slot_words(L, p.sx) * 4;
+    return 128 + (size_t)9 * lf_of(L, p.sx) * 4 + (size_t)p.nslot * slot_words(L, p.sx) * 4 + WT_BYTES;
   };
   const size_t min_slot = (size_t)(9 * 8 * (ppc_mean + 4.0)) * 16 + 1024;  // ~8 cells' windows
   while (p.L > 8 && fixed_of(p.L) + (size_t)p.nslot * min_slot > max_smem) p.L = (p.L + 1) / 2;
-  p.nseg = (own + p.L - 1) / p.L;
-  p.nitems = (long long)p.nseg * g.ny * g.nz;
+  segs();
   int cap = a.tx_cap;
   if (cap <= 0) {
     // every slot as large as shared memory allows (one block per SM either way): rows through

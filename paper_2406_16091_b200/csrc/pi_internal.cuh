@@ -260,6 +260,9 @@ struct InteractArgs {
   int tpl;                      // tuning (x-pencil): targets per lane (0 = default)
   int32_t *dense;               // [ncells] cells listed by the X-pencil for the Par-Cell-SM pass
   int fb[3], fb_cap;            // tuning (full load)
+  bool xr_set;                  // X-pencil: only the target X layers [xr0, xr1) + [xr2, xr3)
+  int xr[4];                    //   (local; else every owned layer)
+  int reserve_sms;              // X-pencil: SMs left free for kernels overlapping the launch
 };
 
 // Lets `func` use the device's whole opt-in shared memory.  The attribute is process-global

@@ -44,13 +44,13 @@ __device__ __forceinline__ void msg_put(void *msg, long long cap, long long idx,
   }
 }
 
-__global__ void k_reset(void *sL, void *sR, void *rL, void *rR, DevCtl *ctl) {
+__global__ void k_reset(void *sL, void *sR, void *rL, void *rR, DevCtl *ctl, bool stay) {
   if (threadIdx.x == 0) {
     if (sL) reinterpret_cast<MsgHeader *>(sL)->count = 0;
     if (sR) reinterpret_cast<MsgHeader *>(sR)->count = 0;
     if (rL) reinterpret_cast<MsgHeader *>(rL)->count = 0;
     if (rR) reinterpret_cast<MsgHeader *>(rR)->count = 0;
-    ctl->n_stay = 0;
+    if (stay) ctl->n_stay = 0;
   }
 }
 
@@ -78,7 +78,8 @@ __global__ void k_soa_to_x(Geom g, int lo, int hi, long long n, const float *__r
 // Owned sorted slots -> stayers (xrec) or migrants (sendL / sendR) by their NEW global cell.
 __global__ void k_migrate(Geom g, long long cap, int rank, int nranks, int Lx, const float4 *__restrict__ rec,
                           const float4 *__restrict__ upd, const int32_t *__restrict__ uid, float4 *xrec,
-                          int32_t *xid, int32_t *xperm, void *sL, void *sR, long long cap_msg, DevCtl *ctl) {
+                          int32_t *xid, int32_t *xperm, void *sL, void *sR, long long cap_msg, DevCtl *ctl,
+                          bool send) {
   const long long n = ctl->n_total;
   const int lo = rank * Lx, hi = (rank + 1) * Lx;
   bool bad = false;
@@ -97,9 +98,20 @@ __global__ void k_migrate(Geom g, long long cap, int rank, int nranks, int Lx, c
         const int cg = cell_coord(u.x, g.ox, g.inv_w, g.gnx, bad);
         cls = cg < lo ? 1 : (cg >= hi ? 2 : 0);
         bad |= (cg < lo - Lx) || (cg >= hi + Lx) || (cls == 1 && rank == 0) || (cls == 2 && rank == nranks - 1);
+        // overlapped step: a particle now in a boundary layer must come from the 2 layers the
+        // boundary launch computed (its ghost copy was taken from there)
+        if (!send) bad |= (cg == lo || cg == hi - 1) && cx >= g.own_lo + 2 && cx < g.own_hi - 2;
       }
     }
     const long long is = agg_append(cls == 0, &ctl->n_stay);
+    if (!send) {
+      if (cls == 0 && is < cap) {
+        xrec[is] = u;
+        xid[is] = id;
+        xperm[is] = -1;
+      }
+      continue;
+    }
     const long long il = agg_append(cls == 1, &reinterpret_cast<MsgHeader *>(sL)->count);
     const long long ir = agg_append(cls == 2, &reinterpret_cast<MsgHeader *>(sR)->count);
     if (cls == 0 && is < cap) {
@@ -111,6 +123,71 @@ __global__ void k_migrate(Geom g, long long cap, int rank, int nranks, int Lx, c
     if (cls == 2) msg_put(sR, cap_msg, ir, u, id);
   }
   if (bad) atomicOr(&ctl->flags, FLAG_INTERNAL);
+}
+
+// Overlapped step, after the boundary launch: the particles of the first / last 2 owned layers
+// (old cell) -> leavers into the migrant messages (set 0), stayers whose new cell is the first /
+// last owned layer into the ghost messages (set 1) for rank-1 / rank+1.
+__global__ void k_migrate_boundary(Geom g, int rank, int nranks, int Lx, const float4 *__restrict__ rec,
+                                   const float4 *__restrict__ upd, const int32_t *__restrict__ uid, MsgSet m,
+                                   MsgSet gh, long long cap_msg, DevCtl *ctl) {
+  const long long n = ctl->n_total;
+  const int lo = rank * Lx, hi = (rank + 1) * Lx;
+  bool bad = false;
+  for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < n; t0 += (long long)gridDim.x * blockDim.x) {
+    const long long t = t0 + threadIdx.x;
+    int cls = -1;  // 0 stay (ghost L), 1 left, 2 right, 3 stay (ghost R)
+    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t id = 0;
+    if (t < n) {
+      const int cx = cell_x(g, rec[t].x, bad);
+      const bool bnd = (cx >= g.own_lo && cx < g.own_lo + 2) || (cx >= g.own_hi - 2 && cx < g.own_hi);
+      if (bnd) {
+        u = upd[t];
+        id = uid[t];
+        const int cg = cell_coord(u.x, g.ox, g.inv_w, g.gnx, bad);
+        cls = cg < lo ? 1 : (cg >= hi ? 2 : (cg == lo && rank > 0 ? 0 : (cg == hi - 1 && rank < nranks - 1 ? 3 : -1)));
+      }
+    }
+    const long long il = agg_append(cls == 1, &reinterpret_cast<MsgHeader *>(m.sendL)->count);
+    const long long ir = agg_append(cls == 2, &reinterpret_cast<MsgHeader *>(m.sendR)->count);
+    const long long gl = agg_append(cls == 0, &reinterpret_cast<MsgHeader *>(gh.sendL)->count);
+    const long long gr = agg_append(cls == 3, &reinterpret_cast<MsgHeader *>(gh.sendR)->count);
+    if (cls == 1) msg_put(m.sendL, cap_msg, il, u, id);
+    if (cls == 2) msg_put(m.sendR, cap_msg, ir, u, id);
+    if (cls == 0) msg_put(gh.sendL, cap_msg, gl, u, id);
+    if (cls == 3) msg_put(gh.sendR, cap_msg, gr, u, id);
+  }
+  if (bad) atomicOr(&ctl->flags, FLAG_INTERNAL);
+}
+
+// ... and the migrants that arrived (they land in the first / last owned layer: |dx| < w) ->
+// ghost messages of the same side (an arrival from rank-1 is a ghost for rank-1 again).
+__global__ void k_ghost_arrivals(Geom g, int rank, int nranks, int Lx, MsgSet m, MsgSet gh, long long cap_msg,
+                                 DevCtl *ctl) {
+  const long long cl = m.recvL ? min(reinterpret_cast<const MsgHeader *>(m.recvL)->count, cap_msg) : 0;
+  const long long cr = m.recvR ? min(reinterpret_cast<const MsgHeader *>(m.recvR)->count, cap_msg) : 0;
+  const int lo = rank * Lx, hi = (rank + 1) * Lx;
+  bool bad = false;
+  for (long long k0 = (long long)blockIdx.x * blockDim.x; k0 < cl + cr; k0 += (long long)gridDim.x * blockDim.x) {
+    const long long k = k0 + threadIdx.x;
+    int cls = -1;
+    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t id = 0;
+    if (k < cl + cr) {
+      void *msg = k < cl ? m.recvL : m.recvR;
+      const long long j = k < cl ? k : k - cl;
+      u = msg_rec(msg)[j];
+      id = msg_id(msg, cap_msg)[j];
+      const int cg = cell_coord(u.x, g.ox, g.inv_w, g.gnx, bad);
+      cls = (cg == lo && rank > 0) ? 0 : ((cg == hi - 1 && rank < nranks - 1) ? 3 : -1);
+    }
+    const long long gl = agg_append(cls == 0, &reinterpret_cast<MsgHeader *>(gh.sendL)->count);
+    const long long gr = agg_append(cls == 3, &reinterpret_cast<MsgHeader *>(gh.sendR)->count);
+    if (cls == 0) msg_put(gh.sendL, cap_msg, gl, u, id);
+    if (cls == 3) msg_put(gh.sendR, cap_msg, gr, u, id);
+  }
+  (void)bad;
 }
 
 // Appends the records of recvL then recvR at *counter; *result = *counter + arrivals.
@@ -242,22 +319,23 @@ struct LocalTransport : Transport {
       delete grp;
     }
   }
-  cudaError_t run(SlabState &S, cudaStream_t s, const Xfer *L, int nL, const Xfer *R, int nR) override {
+  cudaError_t run(SlabState &S, int set, cudaStream_t s, const Xfer *L, int nL, const Xfer *R, int nR) override {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return e;
     if (!grp->barrier()) return cudaErrorTimeout;  // every rank's send buffers are complete
     auto u8 = [](void *p, size_t o) { return static_cast<unsigned char *>(p) + o; };
+    const MsgSet me = S.set(set);
     if (S.rank > 0) {
-      SlabState *P = grp->members[S.rank - 1];
+      const MsgSet P = grp->members[S.rank - 1]->set(set);
       for (int k = 0; k < nL && e == cudaSuccess; ++k)
         if (L[k].rbytes)
-          e = cudaMemcpyAsync(u8(S.recvL, L[k].off), u8(P->sendR, L[k].off), L[k].rbytes, cudaMemcpyDeviceToDevice, s);
+          e = cudaMemcpyAsync(u8(me.recvL, L[k].off), u8(P.sendR, L[k].off), L[k].rbytes, cudaMemcpyDeviceToDevice, s);
     }
     if (S.rank < S.nranks - 1) {
-      SlabState *P = grp->members[S.rank + 1];
+      const MsgSet P = grp->members[S.rank + 1]->set(set);
       for (int k = 0; k < nR && e == cudaSuccess; ++k)
         if (R[k].rbytes)
-          e = cudaMemcpyAsync(u8(S.recvR, R[k].off), u8(P->sendL, R[k].off), R[k].rbytes, cudaMemcpyDeviceToDevice, s);
+          e = cudaMemcpyAsync(u8(me.recvR, R[k].off), u8(P.sendL, R[k].off), R[k].rbytes, cudaMemcpyDeviceToDevice, s);
     }
     if (e != cudaSuccess) return e;
     e = cudaStreamSynchronize(s);
@@ -317,20 +395,21 @@ struct NcclTransport : Transport {
   ~NcclTransport() override {
     if (comm) g_nccl.destroy(comm);
   }
-  cudaError_t run(SlabState &S, cudaStream_t s, const Xfer *L, int nL, const Xfer *R, int nR) override {
+  cudaError_t run(SlabState &S, int set, cudaStream_t s, const Xfer *L, int nL, const Xfer *R, int nR) override {
     constexpr int ncclChar = 0;
     auto u8 = [](void *p, size_t o) { return static_cast<unsigned char *>(p) + o; };
+    const MsgSet m = S.set(set);
     if (g_nccl.gstart() != 0) return cudaErrorUnknown;
     bool ok = true;
     if (S.rank > 0)
       for (int k = 0; k < nL; ++k) {
-        if (L[k].sbytes) ok &= g_nccl.send(u8(S.sendL, L[k].off), L[k].sbytes, ncclChar, S.rank - 1, comm, s) == 0;
-        if (L[k].rbytes) ok &= g_nccl.recv(u8(S.recvL, L[k].off), L[k].rbytes, ncclChar, S.rank - 1, comm, s) == 0;
+        if (L[k].sbytes) ok &= g_nccl.send(u8(m.sendL, L[k].off), L[k].sbytes, ncclChar, S.rank - 1, comm, s) == 0;
+        if (L[k].rbytes) ok &= g_nccl.recv(u8(m.recvL, L[k].off), L[k].rbytes, ncclChar, S.rank - 1, comm, s) == 0;
       }
     if (S.rank < S.nranks - 1)
       for (int k = 0; k < nR; ++k) {
-        if (R[k].sbytes) ok &= g_nccl.send(u8(S.sendR, R[k].off), R[k].sbytes, ncclChar, S.rank + 1, comm, s) == 0;
-        if (R[k].rbytes) ok &= g_nccl.recv(u8(S.recvR, R[k].off), R[k].rbytes, ncclChar, S.rank + 1, comm, s) == 0;
+        if (R[k].sbytes) ok &= g_nccl.send(u8(m.sendR, R[k].off), R[k].sbytes, ncclChar, S.rank + 1, comm, s) == 0;
+        if (R[k].rbytes) ok &= g_nccl.recv(u8(m.recvR, R[k].off), R[k].rbytes, ncclChar, S.rank + 1, comm, s) == 0;
       }
     ok &= g_nccl.gend() == 0;
     return ok ? cudaSuccess : cudaErrorUnknown;
@@ -340,17 +419,18 @@ struct NcclTransport : Transport {
 
 }  // namespace
 
-cudaError_t slab_exchange(SlabState &S, cudaStream_t s) {
+cudaError_t slab_exchange(SlabState &S, cudaStream_t s, int set) {
   const bool hasL = S.rank > 0, hasR = S.rank < S.nranks - 1;
   if (!S.counted || !S.hcnt) {  // the whole fixed-capacity messages, no host synchronisation
     const Xfer x{0, msg_bytes(S.cap_msg), msg_bytes(S.cap_msg)};
     S.bytes_sent += (long long)x.sbytes * (hasL + hasR);
-    return S.tr->run(S, s, &x, hasL, &x, hasR);
+    return S.tr->run(S, set, s, &x, hasL, &x, hasR);
   }
   // phase 1: the headers (counts)
   const Xfer h{0, sizeof(MsgHeader), sizeof(MsgHeader)};
-  cudaError_t e = S.tr->run(S, s, &h, hasL, &h, hasR);
-  void *hd[4] = {S.sendL, S.sendR, S.recvL, S.recvR};
+  cudaError_t e = S.tr->run(S, set, s, &h, hasL, &h, hasR);
+  const MsgSet m = S.set(set);
+  void *hd[4] = {m.sendL, m.sendR, m.recvL, m.recvR};
   for (int k = 0; k < 4 && e == cudaSuccess; ++k)
     e = cudaMemcpyAsync(S.hcnt + k, hd[k], sizeof(long long), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -363,7 +443,7 @@ cudaError_t slab_exchange(SlabState &S, cudaStream_t s) {
   const Xfer L[2] = {{o_rec, sl * 16, rl * 16}, {o_id, sl * 4, rl * 4}};
   const Xfer R[2] = {{o_rec, sr * 16, rr * 16}, {o_id, sr * 4, rr * 4}};
   S.bytes_sent += (long long)((sl + sr) * 20 + sizeof(MsgHeader) * (hasL + hasR));
-  return S.tr->run(S, s, L, hasL ? 2 : 0, R, hasR ? 2 : 0);
+  return S.tr->run(S, set, s, L, hasL ? 2 : 0, R, hasR ? 2 : 0);
 }
 
 bool nccl_unique_id(void *out128, char *why, size_t n) {
@@ -412,8 +492,9 @@ Transport *make_transport(const pi_config *cfg, SlabState *S, char *why, size_t 
   return t;
 }
 
-cudaError_t slab_reset(SlabState &S, DevCtl *ctl, cudaStream_t s) {
-  k_reset<<<1, 32, 0, s>>>(S.sendL, S.sendR, S.recvL, S.recvR, ctl);
+cudaError_t slab_reset(SlabState &S, DevCtl *ctl, cudaStream_t s, int set, bool stay) {
+  const MsgSet m = S.set(set);
+  k_reset<<<1, 32, 0, s>>>(m.sendL, m.sendR, m.recvL, m.recvR, ctl, stay);
   return cudaGetLastError();
 }
 
@@ -425,17 +506,36 @@ cudaError_t slab_from_soa(SlabState &S, const Geom &g, long long n, const float 
 }
 
 cudaError_t slab_migrate(SlabState &S, const Geom &g, long long cap, const float4 *rec, const float4 *upd,
-                         const int32_t *uid, DevCtl *ctl, cudaStream_t s) {
+                         const int32_t *uid, DevCtl *ctl, cudaStream_t s, bool send) {
   k_migrate<<<blocks_for(cap), T, 0, s>>>(g, cap, S.rank, S.nranks, S.Lx, rec, upd, uid, S.xrec, S.xid, S.xperm,
-                                          S.sendL, S.sendR, S.cap_msg, ctl);
+                                          S.sendL, S.sendR, S.cap_msg, ctl, send);
+  return cudaGetLastError();
+}
+
+cudaError_t slab_migrate_boundary(SlabState &S, const Geom &g, long long cap, const float4 *rec, const float4 *upd,
+                                  const int32_t *uid, DevCtl *ctl, cudaStream_t s) {
+  // a few blocks: they run beside the interior launch (on the SMs it leaves free, or in the
+  // registers and threads its blocks leave on every SM)
+  k_migrate_boundary<<<min(blocks_for(cap), 148 * 2), T, 0, s>>>(g, S.rank, S.nranks, S.Lx, rec, upd, uid, S.set(0),
+                                                                 S.set(1), S.cap_msg, ctl);
+  return cudaGetLastError();
+}
+
+cudaError_t slab_ghost_arrivals(SlabState &S, const Geom &g, DevCtl *ctl, cudaStream_t s) {
+  const bool l = S.rank > 0, r = S.rank < S.nranks - 1;
+  MsgSet m = S.set(0);
+  if (!l) m.recvL = nullptr;
+  if (!r) m.recvR = nullptr;
+  k_ghost_arrivals<<<blocks_for(2 * S.cap_msg), T, 0, s>>>(g, S.rank, S.nranks, S.Lx, m, S.set(1), S.cap_msg, ctl);
   return cudaGetLastError();
 }
 
 cudaError_t slab_append(SlabState &S, long long *counter, long long *result, long long *stat, long long *out_stat,
-                        long long cap, DevCtl *ctl, cudaStream_t s) {
+                        long long cap, DevCtl *ctl, cudaStream_t s, int set) {
   const bool l = S.rank > 0, r = S.rank < S.nranks - 1;
-  k_append<<<blocks_for(2 * S.cap_msg), T, 0, s>>>(l ? S.recvL : nullptr, r ? S.recvR : nullptr, l ? S.sendL : nullptr,
-                                                   r ? S.sendR : nullptr, S.cap_msg, counter, result, stat, out_stat,
+  const MsgSet m = S.set(set);
+  k_append<<<blocks_for(2 * S.cap_msg), T, 0, s>>>(l ? m.recvL : nullptr, r ? m.recvR : nullptr, l ? m.sendL : nullptr,
+                                                   r ? m.sendR : nullptr, S.cap_msg, counter, result, stat, out_stat,
                                                    cap, S.xrec, S.xid, S.xperm, ctl);
   return cudaGetLastError();
 }

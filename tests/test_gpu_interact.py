@@ -142,7 +142,9 @@ def test_xpencil_tuning_shapes(algo):
                  dict(xpencil_cap=16), dict(xpencil_slots=3), dict(xpencil_slots=4, xpencil_len=16),
                  dict(xpencil_slots=4, threads=256), dict(xpencil_slots=5),
                  dict(xpencil_targets=2), dict(xpencil_targets=2, xpencil_len=7, xpencil_cap=300),
-                 dict(xpencil_targets=2, xpencil_cap=64), dict(xpencil_targets=2, threads=288)):
+                 dict(xpencil_targets=2, xpencil_cap=64), dict(xpencil_targets=2, threads=288),
+                 dict(xpencil_targets=3), dict(xpencil_targets=3, xpencil_len=7, xpencil_cap=300),
+                 dict(xpencil_targets=3, xpencil_cap=64), dict(xpencil_targets=3, threads=288)):
         got, ctx = gpu_interact(c, algo, tuning=tune)
         assert_parity(got, want, label=f"{algo} {tune}")
         if algo == "xpencil" and tune.get("xpencil_cap") in (16, 64):

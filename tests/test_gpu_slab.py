@@ -112,12 +112,18 @@ def test_slab_binning_counts_exact():
         assert offsets[-1] == counts.sum()
 
 
-@pytest.mark.parametrize("algo", ["xpencil", "global", "half"])
-def test_slab_steps_migrate_and_match_oracle(algo):
+@pytest.mark.parametrize("algo,P,overlap", [("xpencil", 4, 0), ("xpencil", 2, 0), ("xpencil", 4, 1),
+                                             ("xpencil", 2, 1), ("global", 4, 0), ("half", 4, 0)])
+def test_slab_steps_migrate_and_match_oracle(algo, P, overlap):
+    """Several steps with migration every step.  X-pencil: overlap 0 (default) computes the 2
+    boundary layers per side first and exchanges migrants and ghosts on a second stream during
+    the interior launch (P = 2: 8 owned layers, an interior launch; P = 4: 4 layers, none);
+    overlap 1 exchanges serially at the start of the next step."""
     c = synth.make_config("c0", n=4 * 4096)
     g = c.grid
-    P = 4
     ctxs = _contexts(g, P, capacity=c.n)
+    for k in ctxs:
+        k.set_tuning(exchange_overlap=overlap)
     parts = [_partition(c, k) for k in ctxs]
     # dt so that the fastest particle moves ~0.8 cell per step: migration every step
     F = celllist.interact(c.x, c.y, c.z, c.q, g)["out"][:, 1:]
@@ -169,6 +175,8 @@ def test_slab_steps_migrate_and_match_oracle(algo):
         # the next step re-bins: every rank owns exactly the particles in its slab
         _all(pool, step, ctxs)
         st = _all(pool, state, ctxs)
+    for _, stats in st:
+        assert stats["overlapped_steps"] == (4 if algo == "xpencil" and overlap == 0 else 0)
     cx = celllist.cells(s0["x"], s0["y"], s0["z"], g) % g.dims[0]
     for r, (s, stats) in enumerate(st):
         sl = ctxs[r].slab
