@@ -165,7 +165,18 @@ __device__ __forceinline__ void take_offsets(const XpParams &p, const Slot &sl, 
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncwarp();
   const int n = 9 * lf_of(p.L, p.sx);
-  for (int k = threadIdx.x & 31; k < n; k += 32) sl.O[k] = stage[k];
+  // 8 loads, then 8 stores: the slot and the stage are both shared memory, so the compiler
+  // cannot reorder a load above a store it might alias -- one at a time, every load's latency
+  // was exposed
+  int k = threadIdx.x & 31;
+  for (; k + 7 * 32 < n; k += 8 * 32) {
+    int v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = stage[k + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) sl.O[k + 32 * u] = v[u];
+  }
+  for (; k < n; k += 32) sl.O[k] = stage[k];
   __syncwarp();
 }
 
