@@ -71,36 +71,37 @@ struct XpParams {
   int reserve;       // SMs left free (the exchange kernels overlapping this launch)
 };
 
-// Slot: SA[capp] | SB[capp] float4 (source pairs, planes A and B) | meta[16] | O[9][LF] | rb[32],
-// LF = (L+2) sx + 1
-//   O[r][k]  global offsets of pencil r (= (dy + 1) + 3 (dz + 1)) at the fine (X sub-cell)
-//            boundary k of the cells x0-1 .. x0+L; the cell boundary j is O[r][j sx]
+// Shared memory: header (mbarriers, O-table item indices) | nslot slots | NOB = nslot + 1
+// offsets tables O[9][LF] | the cell-group consumers' run tables.
+// Slot: SA[capp] | SB[capp] float4 (source pairs, planes A and B) | meta[16] | rb[32]
 //   rb[r]    first staged pair of pencil r's run in S (rb[9] = total); rb[16 + r] = rb[r] minus
 //            the global pair index of the run's first record: staged pair of global pair k
 // meta: 0 stop (1), 1 ja, 2 jb (target cells ja..jb of the item in this round; an empty round
-//       has ntargets = 0), 3 ntargets, 4 x0, 5 cy | cz << 16, 6 batch counter
+//       has ntargets = 0), 3 ntargets, 4 x0, 5 cy | cz << 16, 6 batch counter, 7 O table
+// O table (LF = (L+2) sx + 1): O[r][k] = global offset of pencil r (= (dy + 1) + 3 (dz + 1)) at
+//   the fine (X sub-cell) boundary k of the cells x0-1 .. x0+L; the cell boundary j is O[r][j sx].
+//   Filled by the helper warp one item ahead; the slots of an item's rounds share its table.
+constexpr int HDR = 256;
 __host__ __device__ inline int lf_of(int L, int sx) { return (L + 2) * sx + 1; }
-__host__ __device__ inline int slot_words(int L, int sx) { return (META + 9 * lf_of(L, sx) + 32 + 3) & ~3; }
-__host__ __device__ inline size_t slot_bytes(int L, int capp, int sx) {
-  return (size_t)capp * 32 + (size_t)slot_words(L, sx) * 4;
-}
+__host__ __device__ inline int slot_words() { return (META + 32 + 3) & ~3; }
+__host__ __device__ inline size_t slot_bytes(int capp) { return (size_t)capp * 32 + (size_t)slot_words() * 4; }
+__host__ __device__ inline size_t otab_bytes(int L, int sx) { return ((size_t)9 * lf_of(L, sx) * 4 + 15) & ~size_t(15); }
 __host__ __device__ inline size_t xp_smem_bytes(int L, int capp, int sx, int nslot) {
-  // + offsets staging + the cell-group consumers' run tables (32 ints per warp, <= 20 warps)
-  return 128 + nslot * slot_bytes(L, capp, sx) + (size_t)9 * lf_of(L, sx) * 4 + WT_BYTES;
+  return HDR + nslot * slot_bytes(capp) + (size_t)(nslot + 1) * otab_bytes(L, sx) + WT_BYTES;
 }
 
 struct Slot {
   float4 *S, *SB;  // planes A (x, y) and B (z, q) of the staged source pairs
   int *meta, *O, *rb;
 };
-__device__ __forceinline__ Slot slot_at(unsigned char *base, int L, int capp, int sx, int s) {
-  unsigned char *u = base + (size_t)s * slot_bytes(L, capp, sx);
+__device__ __forceinline__ Slot slot_at(unsigned char *base, int capp, int s) {
+  unsigned char *u = base + (size_t)s * slot_bytes(capp);
   Slot sl;
   sl.S = reinterpret_cast<float4 *>(u);
   sl.SB = sl.S + capp;
   sl.meta = reinterpret_cast<int *>(u + (size_t)capp * 32);
-  sl.O = sl.meta + META;
-  sl.rb = sl.O + 9 * lf_of(L, sx);
+  sl.rb = sl.meta + META;
+  sl.O = nullptr;
   return sl;
 }
 
@@ -124,10 +125,10 @@ __global__ void k_pairify(long long n, const long long *n_dev, const float4 *__r
 }
 
 // ---------------------------------------------------------------- producer (one warp)
-// The producer's next item: its offset tables are fetched with cp.async into a staging
-// table while the current item is computed, then copied into the slot (the global-load
-// latency is otherwise on the critical path of every slot refill: measured, consumers found
-// a third of the slots not yet filled).
+// The offsets tables are fetched by a helper warp, one item ahead of the producer, straight into
+// the table the slots of that item will use (XP_PROFILE: with the fetch and a copy into the slot
+// in the producer's own loop, the producer's ~18K cycles per item set the pace and the consumer
+// warps waited ~12 % of their time for a slot).
 __device__ __forceinline__ void item_geom(const XpParams &p, long long item, int &x0, int &Lseg, int &cy, int &cz) {
   const int seg = (int)(item % p.nseg);
   const long long row = item / p.nseg;
@@ -161,25 +162,6 @@ __device__ __forceinline__ void prefetch_offsets(const XpParams &p, long long it
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void take_offsets(const XpParams &p, const Slot &sl, const int *stage) {
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncwarp();
-  const int n = 9 * lf_of(p.L, p.sx);
-  // 8 loads, then 8 stores: the slot and the stage are both shared memory, so the compiler
-  // cannot reorder a load above a store it might alias -- one at a time, every load's latency
-  // was exposed
-  int k = threadIdx.x & 31;
-  for (; k + 7 * 32 < n; k += 8 * 32) {
-    int v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = stage[k + 32 * u];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) sl.O[k + 32 * u] = v[u];
-  }
-  for (; k < n; k += 32) sl.O[k] = stage[k];
-  __syncwarp();
-}
-
 // Round [ja, jb] of the item: the largest jb <= Lseg whose 9 pencil runs (cells ja-1 .. jb+1,
 // whole source pairs) fit the slot (warp-uniform; jb < ja: cell ja alone does not fit).
 __device__ int choose_round(const XpParams &p, const Slot &sl, int ja, int Lseg) {
@@ -362,13 +344,19 @@ __device__ __forceinline__ float4 walk_flat(const Slot &sl, const int *wt, int N
 // UPD: pi_step (update + carried counts in the epilogue); TPL: targets per lane (1: walk9,
 // 2: walk9x2), 0: cell groups (walk_flat)
 template <int KERNEL, int NC, bool UPD, int TPL>
-__global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams p) {
+__global__ void __launch_bounds__((NC + 2) * 32, 1) k_interact_xpencil(XpParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int NSLOT = p.nslot;
+  const int NSLOT = p.nslot, NOB = NSLOT + 1;
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem_raw);  // [nslot]
   unsigned long long *empty = full + MAX_SLOTS;                                  // [nslot]
-  unsigned char *slots = smem_raw + 128;
+  unsigned long long *ofull = empty + MAX_SLOTS;                                 // [nslot + 1]
+  unsigned long long *oempty = ofull + MAX_SLOTS + 1;                            // [nslot + 1]
+  int *obitem = reinterpret_cast<int *>(oempty + MAX_SLOTS + 1);                 // [nslot + 1]
+  int *olast = obitem + MAX_SLOTS + 1;                                           // [nslot + 1]
+  unsigned char *slots = smem_raw + HDR;
   const int L = p.L, sx = p.sx, LF = lf_of(L, sx);
+  int *obufs = reinterpret_cast<int *>(slots + (size_t)NSLOT * slot_bytes(p.capp));
+  const int OBW = (int)(otab_bytes(L, sx) / 4);
   const Geom &g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned long long cand = 0, fallbacks = 0;
@@ -378,30 +366,61 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       mbar_init(&full[k], 1);    // producer lane 0 (arrive.expect_tx) + the TMA bytes
       mbar_init(&empty[k], NC);  // one arrival per consumer warp
     }
+    for (int k = 0; k < NOB; ++k) {
+      mbar_init(&ofull[k], 1);   // helper lane 0, after its copies landed
+      mbar_init(&oempty[k], 1);  // producer lane 0, once the slots using the table are released
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == NC) {
+  if (warp == NC + 1) {
+    // ================================ helper: offsets tables ================================
+    for (int i = 0;; ++i) {
+      const int b = i % NOB;
+      if (i >= NOB) mbar_wait_sleep(&oempty[b], ((i / NOB) - 1) & 1);
+      long long item = 0;
+      if (lane == 0) item = (long long)atomicAdd(&p.ctl->xp_items, 1ull);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      const bool stop = item >= p.nitems;
+      if (!stop) {
+        prefetch_offsets(p, item, obufs + (size_t)b * OBW);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncwarp();
+      if (lane == 0) {
+        obitem[b] = stop ? -1 : (int)item;
+        mbar_arrive(&ofull[b]);  // release: the table (and the item index)
+      }
+      if (stop) break;
+    }
+  } else if (warp == NC) {
     // ================================ producer ================================
-    long long item = -1, next = 0;
+    long long item = -1;
     int x0 = 0, Lseg = 0, cy = 0, cz = 0, ja = 1;
-    int *stage = reinterpret_cast<int *>(slots + (size_t)NSLOT * slot_bytes(L, p.capp, sx));
-    if (lane == 0) next = (long long)atomicAdd(&p.ctl->xp_items, 1ull);
-    next = __shfl_sync(0xffffffffu, next, 0);
-    if (next < p.nitems) prefetch_offsets(p, next, stage);
+    int taken = 0, freed = 0, ob = 0;  // tables received / released; the current item's table
     for (unsigned use = 0;; ++use) {
       const int s = use % NSLOT;
-      const Slot sl = slot_at(slots, L, p.capp, sx, s);
+      Slot sl = slot_at(slots, p.capp, s);
       XP_T(t0);
-      if (use >= NSLOT) mbar_wait_sleep(&empty[s], ((use / NSLOT) - 1) & 1);  // consumers released it
+      if (use >= NSLOT) {
+        mbar_wait_sleep(&empty[s], ((use / NSLOT) - 1) & 1);  // consumers released it
+        // every use up to use - NSLOT is released: free the tables no later use refers to
+        while (freed < taken && olast[freed % NOB] <= (int)(use - NSLOT)) {
+          if (lane == 0) mbar_arrive(&oempty[freed % NOB]);
+          ++freed;
+        }
+      }
       XP_T(t1);
       XP_ADD(0, t0, t1);
       fence_proxy_async();  // their generic reads of the slot precede the TMA writes below
       const bool fresh = item < 0 || ja > Lseg;
       if (fresh) {
-        item = next;
-        if (item >= p.nitems) {  // stop marker: consumers leave at the first one
+        ob = taken % NOB;
+        mbar_wait_sleep(&ofull[ob], (taken / NOB) & 1);
+        ++taken;
+        item = obitem[ob];
+        if (item < 0) {  // stop marker: consumers leave at the first one
           if (lane == 0) {
             sl.meta[0] = 1;
             mbar_arrive(&full[s]);
@@ -409,14 +428,11 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
           break;
         }
         item_geom(p, item, x0, Lseg, cy, cz);
-        take_offsets(p, sl, stage);
         ja = 1;
-      } else {
-        // next round of the same item: the offsets are reused (copy them into this slot)
-        const Slot prev = slot_at(slots, L, p.capp, sx, (use - 1) % NSLOT);
-        for (int k = lane; k < 9 * LF; k += 32) sl.O[k] = prev.O[k];
-        __syncwarp();
       }
+      // (a next round of the same item reuses its table)
+      sl.O = obufs + (size_t)ob * OBW;
+      if (lane == 0) olast[ob] = (int)use;
       int jb = choose_round(p, sl, ja, Lseg);
       // a cell whose window alone does not fit the slot is listed for the Par-Cell-SM pass
       // (interact_cellsm.cu) and skipped; an item that ends in such cells leaves an empty round
@@ -467,6 +483,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         sl.meta[4] = x0;
         sl.meta[5] = cy | (cz << 16);
         sl.meta[6] = 0;
+        sl.meta[7] = ob;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&full[s], (unsigned)total * 32u);  // release: tables
@@ -476,11 +493,6 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
         bulk_g2s(sl.SB + (incl - len), p.pairs + p.plane + a, (unsigned)len * 16u, &full[s]);
       }
       ja = last + 1;
-      if (fresh) {  // the slot is on its way: fetch the following item's offsets meanwhile
-        if (lane == 0) next = (long long)atomicAdd(&p.ctl->xp_items, 1ull);
-        next = __shfl_sync(0xffffffffu, next, 0);
-        if (next < p.nitems) prefetch_offsets(p, next, stage);
-      }
       XP_T(t2);
       XP_ADD(1, t1, t2);
       XP_ADD(2, 0, 1);
@@ -493,12 +505,13 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     const float thr = __shfl_sync(0xffffffffu, p.kp.rc2, 0), mc2 = __shfl_sync(0xffffffffu, -p.kp.c2, 0);
     for (unsigned use = 0;; ++use) {
       const int s = use % NSLOT;
-      const Slot sl = slot_at(slots, L, p.capp, sx, s);
+      Slot sl = slot_at(slots, p.capp, s);
       XP_T(c0);
       mbar_wait(&full[s], (use / NSLOT) & 1);
       XP_T(c1);
       XP_ADD(3, c0, c1);
       if (sl.meta[0]) break;  // out of work items
+      sl.O = obufs + (size_t)sl.meta[7] * OBW;
       const int ja = sl.meta[1], jb = sl.meta[2], ntargets = sl.meta[3], x0 = sl.meta[4];
       const int cy = sl.meta[5] & 0xffff, cz = sl.meta[5] >> 16;
       const int *O4 = sl.O + 4 * LF;  // home pencil; cell boundary j at O4[j sx]
@@ -542,8 +555,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
       };
       if (TPL == 0) {
         // cell groups: a batch is one target cell j of the round (in chunks of <= 32 targets)
-        int *wt = reinterpret_cast<int *>(slots + (size_t)NSLOT * slot_bytes(L, p.capp, sx) +
-                                          (size_t)9 * LF * 4) + warp * 32;
+        int *wt = obufs + (size_t)NOB * OBW + warp * 32;
         for (;;) {
           int b = 0;
           if (lane == 0) b = atomicAdd(&sl.meta[6], 1);
@@ -661,7 +673,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     cp.out = p.out;
     cp.ctl = p.ctl;
     cp.from_rec = false;
-    cellsm_phase<KERNEL, UPD, (NC + 1) * 32>(cp, slots);
+    cellsm_phase<KERNEL, UPD, (NC + 2) * 32>(cp, slots);
   }
 
   // statistics: warp-level sums, spread over CAND_SLOTS counters
@@ -671,26 +683,27 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) k_interact_xpencil(XpParams 
     fallbacks += __shfl_xor_sync(0xffffffffu, fallbacks, o);
   }
   if (lane == 0) {
-    if (cand) atomicAdd(&p.ctl->cand_slots[(blockIdx.x * (NC + 1) + warp) & (CAND_SLOTS - 1)], cand);
+    if (cand) atomicAdd(&p.ctl->cand_slots[(blockIdx.x * (NC + 2) + warp) & (CAND_SLOTS - 1)], cand);
     if (fallbacks) atomicAdd(&p.ctl->fallback_cells, fallbacks);
   }
 }
 
 template <int NC>
 cudaError_t launch_nc(const XpParams &p, cudaStream_t s) {
-  const size_t smem = max(xp_smem_bytes(p.L, p.capp, p.sx, p.nslot), CS_SMEM + 128);
+  const size_t smem = max(xp_smem_bytes(p.L, p.capp, p.sx, p.nslot), CS_SMEM + HDR);
+  constexpr int NT = (NC + 2) * 32;  // consumers, producer, helper
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = allow_max_smem(kern);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (NC + 1) * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
     if (occ < 1) occ = 1;
     long long blocks = (long long)sms * occ - p.reserve;
     if (blocks > p.nitems) blocks = p.nitems;
     if (blocks < 1) blocks = 1;
-    kern<<<(int)blocks, (NC + 1) * 32, smem, s>>>(p);
+    kern<<<(int)blocks, NT, smem, s>>>(p);
     return cudaGetLastError();
   };
   const bool upd = p.out.upd != nullptr;
@@ -811,7 +824,7 @@ cudaError_t launch_interact_xpencil(const Geom &g, const KParams &k, const Inter
   // L = 256 with sx = 16 did not fit at all).  Halve L until two slots hold the windows of a
   // few cells at the mean density.
   auto fixed_of = [&](int L) {
-    return 128 + (size_t)9 * lf_of(L, p.sx) * 4 + (size_t)p.nslot * slot_words(L, p.sx) * 4 + WT_BYTES;
+    return HDR + (size_t)(p.nslot + 1) * otab_bytes(L, p.sx) + (size_t)p.nslot * slot_words() * 4 + WT_BYTES;
   };
   const size_t min_slot = (size_t)(9 * 8 * (ppc_mean + 4.0)) * 16 + 1024;  // ~8 cells' windows
   while (p.L > 8 && fixed_of(p.L) + (size_t)p.nslot * min_slot > max_smem) p.L = (p.L + 1) / 2;
