@@ -9,7 +9,9 @@ relies on, with real ranks and a real transport:
     (the oracle on the whole cloud), because cell_width >= r_c makes one ghost
     layer enough;
   * migration after a position update (|dx| < w) keeps every particle owned exactly once,
-    by the rank whose slab holds its new cell.
+    by the rank whose slab holds its new cell;
+  * the overlapped step's selection (migrants and next ghosts taken from the first / last 2
+    owned layers plus the arrivals) gives the serial protocol's ghost sets.
 Ghost and migrant messages are exchanged with torch.distributed send/recv between two real
 processes; the interactions are the oracle's."""
 import os
@@ -125,6 +127,21 @@ def _worker(rank, port, result_dir):
         acx = celllist.cells(after[0], after[1], after[2], g) % g.dims[0]
         assert np.all((acx >= lo) & (acx < hi))
         moved = int(go_l.sum() + go_r.sum())
+
+        # the overlapped step (pi_tuning.exchange_overlap) takes the migrants and
+        # the next step's ghosts from the particles of the first / last 2 owned layers (their
+        # old cells) plus the arrivals: with |dt F| < w that is every leaver and every particle
+        # that ends in a boundary layer, so its ghost messages equal the serial protocol's
+        # (the first / last owned layer of the state after migration)
+        bnd = (ocx < lo + 2) | (ocx >= hi - 2)
+        assert not np.any((go_l | go_r) & ~bnd), "a leaver outside the boundary layers"
+        arr_ids = np.concatenate([p[4] for _, p in got]) if got else np.zeros(0, np.int32)
+        arr_cx = (celllist.cells(*[np.concatenate([p[k] for _, p in got]) for k in range(3)], g) % g.dims[0]
+                  if len(arr_ids) else np.zeros(0, np.int64))
+        for side, layer in (("L", lo), ("R", hi - 1)):
+            serial = np.sort(after[4][acx == layer])
+            ovl = np.sort(np.concatenate([own[4][bnd & stay & (ncx == layer)], arr_ids[arr_cx == layer]]))
+            assert np.array_equal(serial, ovl), f"overlapped ghost set differs ({side})"
         all_ids = [None] * WORLD
         dist.all_gather_object(all_ids, (after[4].tolist(), moved))
         if rank == 0:
