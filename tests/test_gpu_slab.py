@@ -249,3 +249,57 @@ def test_slab_exchange_counted_bytes():
         nmsg = 3 * ((r > 0) + (r < P - 1))  # pi_bin's ghost exchange + the step's migration and ghosts
         assert st0["exchange_bytes"] >= 20 * st0["migrants_out"] + 16 * nmsg
         assert st0["exchange_bytes"] < st1["exchange_bytes"] / 2  # the counted records, not the capacity
+
+
+def test_slab_overlap_larger_sampled():
+    """The overlapped step at a size with real interior launches and large messages: 2^20 uniform
+    particles on 64^3 cells, P = 4 (16 owned layers per rank), two steps with migration, sampled
+    targets against the oracle on the whole cloud of the pre-step state; the serial exchange
+    gives the same state."""
+    c = synth.scaled_uniform(4, (64, 64, 64), seed=240616099)
+    g = c.grid
+    P = 4
+    F = celllist.interact(c.x, c.y, c.z, c.q, g, targets=np.arange(0, c.n, 97))["out"][:, 1:]
+    dt = float(np.float32(0.4 * g.w / np.abs(F).max()))
+    res = {}
+    for overlap in (0, 1):
+        ctxs = _contexts(g, P, capacity=c.n)
+        parts = [_partition(c, k) for k in ctxs]
+
+        def run(r, k):
+            k.set_tuning(exchange_overlap=overlap)
+            idx = parts[r]
+            with torch.cuda.stream(k.stream):
+                k.bin(*(_dev(a[idx]) for a in (c.x, c.y, c.z, c.q)), id=_dev(idx.astype(np.int32)))
+                k.step("xpencil", dt)
+                p0 = k.get_particles()
+                k.step("xpencil", dt)
+                p1 = k.get_particles()
+            k.stream.synchronize()
+            return ({key: v.cpu().numpy() for key, v in p0.items()}, {key: v.cpu().numpy() for key, v in p1.items()},
+                    k.stats())
+
+        with cf.ThreadPoolExecutor(P) as pool:
+            out = _all(pool, run, ctxs)
+        for k in ctxs:
+            k.close()
+        res[overlap] = out
+        for _, _, st in out:
+            assert st["overlapped_steps"] == (2 if overlap == 0 else 0)
+
+    def union(states):
+        d = {key: np.concatenate([s[key] for s in states]) for key in states[0]}
+        order = np.argsort(d["id"])
+        return {key: v[order] for key, v in d.items()}
+
+    for overlap in (0, 1):
+        s0 = union([o[0] for o in res[overlap]])
+        s1 = union([o[1] for o in res[overlap]])
+        assert np.array_equal(s1["id"], np.arange(c.n)), "a particle lost or duplicated"
+        sample = np.random.default_rng(3).choice(c.n, 4000, replace=False)
+        want = celllist.interact(s0["x"], s0["y"], s0["z"], s0["q"], g, targets=sample)
+        got = np.stack([s1[k][sample] for k in ("phi", "fx", "fy", "fz")], 1).astype(np.float64)
+        assert_parity(got, want, label=f"overlap={overlap} step 2")
+    a, b = union([o[1] for o in res[0]]), union([o[1] for o in res[1]])
+    for key in ("x", "y", "z"):
+        assert np.allclose(a[key], b[key], rtol=0, atol=1e-6 * g.w)
