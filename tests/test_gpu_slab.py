@@ -301,5 +301,5 @@ def test_slab_overlap_larger_sampled():
         got = np.stack([s1[k][sample] for k in ("phi", "fx", "fy", "fz")], 1).astype(np.float64)
         assert_parity(got, want, label=f"overlap={overlap} step 2")
     a, b = union([o[1] for o in res[0]]), union([o[1] for o in res[1]])
-    for key in ("x", "y", "z"):
-        assert np.allclose(a[key], b[key], rtol=0, atol=1e-6 * g.w)
+    for key in ("x", "y", "z"):  # the same state up to the forces' summation order (a few ulp)
+        assert np.allclose(a[key], b[key], rtol=0, atol=1e-6)
