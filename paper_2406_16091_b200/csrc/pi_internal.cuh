@@ -65,12 +65,15 @@ enum : int { FLAG_OUT_OF_BOX = 1, FLAG_CAPACITY = 2, FLAG_INTERNAL = 4, FLAG_DOM
 // ------------------------------------------------------------------------------------
 // a1: cell index, contract C3: c = clamp(floor(fl32(fl32(x - o) * inv_w)), 0, N - 1).
 // __fsub_rn / __fmul_rn forbid FMA contraction, so the result is bit-identical to the
-// per-operation-rounded definition.  NaN maps to cell 0 and raises FLAG_OUT_OF_BOX.
+// per-operation-rounded definition.  A position outside [o, o + N w] (NaN included) maps to
+// the nearest cell and raises FLAG_OUT_OF_BOX (pi.h: positions must lie in the box; the upper
+// face itself clamps into the last cell, with a 2^-20 relative slack for its rounding).
 // ------------------------------------------------------------------------------------
+__device__ __forceinline__ bool outside(float t, int nd) { return !(t >= 0.f && t <= (float)nd * 1.000001f); }
 __device__ __forceinline__ int cell_coord(float x, float o, float inv_w, int nd, bool &bad) {
   float t = __fmul_rn(__fsub_rn(x, o), inv_w);
   float f = floorf(t);
-  bad |= !(f == f);
+  bad |= outside(t, nd);
   int c = (f >= 0.f) ? ((f < (float)nd) ? (int)f : nd - 1) : 0;
   return c;
 }
@@ -94,7 +97,7 @@ __device__ __forceinline__ int cell_lin(const Geom &g, float x, float y, float z
 __device__ __forceinline__ int fine_x_global(const Geom &g, float x, bool &bad) {
   const float t = __fmul_rn(__fsub_rn(x, g.ox), g.inv_w);
   const float f = floorf(t);
-  bad |= !(f == f);
+  bad |= outside(t, g.gnx);
   const int c = (f >= 0.f) ? ((f < (float)g.gnx) ? (int)f : g.gnx - 1) : 0;
   const int sub = min(max((int)((t - (float)c) * (float)g.sx), 0), g.sx - 1);
   return (c << g.sxs) + sub;

@@ -400,3 +400,48 @@ def test_xpencil_interleaved_layout(kernel):
     cl = synth.clustered(1 << 14, synth.Grid(dims=(16, 16, 16), w=1 / 16), seed=240616094)
     got, ctx = gpu_interact(cl, "xpencil", kernel, tuning=dict(xpencil_layout=1, xpencil_cap=200))
     assert_parity(got, oracle_interact(cl, kernel), label=f"interleaved clustered {kernel}")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_xpencil_tuning_fuzz(seed):
+    """Random X-pencil launch shapes (segment length, slot capacity small enough to force rounds
+    and listed dense cells, 2-4 slots, X sub-cells, grid shape, density, kernel) against the
+    oracle: the producer / helper hand-over of offsets tables across rounds and slots, the
+    Par-Cell-SM listing and the windows must give the same sums in every combination."""
+    rng = np.random.default_rng(1000 + seed)
+    dims = tuple(int(v) for v in rng.integers(4, 14, size=3))
+    ppc = float(rng.choice([2, 5, 9, 16]))
+    if seed % 3:
+        c = synth.scaled_uniform(ppc, dims, seed=77 + seed)
+    else:  # clustered blobs in the unit box: a cubic grid of width 1/d (non-dyadic for most d)
+        d = dims[0]
+        c = synth.clustered(int(ppc * d ** 3), synth.Grid(dims=(d, d, d), w=1 / d), seed=88 + seed)
+    kernel = ["gaussian", "indicator", "candidate", "lj"][seed % 4]
+    xs = int(rng.choice([1, 2, 4, 8]))
+    tune = dict(xpencil_len=int(rng.integers(1, 20)), xpencil_cap=int(rng.choice([0, 48, 96, 300, 1000])),
+                xpencil_slots=int(rng.integers(2, 5)))
+    want = oracle_interact(c, kernel)
+    ctx = ctx_for(c, kernel, x_subcells=xs)
+    got, ctx = gpu_interact(c, "xpencil", kernel, tuning=tune, ctx=ctx)
+    assert_parity(got, want, label=f"fuzz {seed} dims {dims} ppc {ppc} sx {xs} {kernel} {tune}")
+    assert ctx.stats()["candidates"] == int(want["C"].sum())
+
+
+def test_out_of_box_flag():
+    """pi.h: a position outside [origin, origin + dims w] raises flag 1 (PI_EDEVICE at the next
+    pi_get_stats); a particle exactly on the upper face is in the box (it clamps into the last
+    cell) and raises nothing."""
+    from paper_2406_16091_b200 import PiError
+    c = synth.make_config("c0")
+    c.x[:8] = 1.0  # the upper face x = 16 w: legal
+    ctx = ctx_for(c)
+    ctx.bin(*to_dev(c))
+    ctx.interact("xpencil")
+    ctx.stats()
+    for bad in (1.0 + 1 / 64, -1e-3, float("nan")):
+        c2 = synth.make_config("c0")
+        c2.y[5] = np.float32(bad)
+        ctx = ctx_for(c2)
+        ctx.bin(*to_dev(c2))
+        with pytest.raises(PiError, match="0x1"):
+            ctx.stats()

@@ -300,6 +300,8 @@ def test_slab_overlap_larger_sampled():
         want = celllist.interact(s0["x"], s0["y"], s0["z"], s0["q"], g, targets=sample)
         got = np.stack([s1[k][sample] for k in ("phi", "fx", "fy", "fz")], 1).astype(np.float64)
         assert_parity(got, want, label=f"overlap={overlap} step 2")
-    a, b = union([o[1] for o in res[0]]), union([o[1] for o in res[1]])
-    for key in ("x", "y", "z"):  # the same state up to the forces' summation order (a few ulp)
+    # after the first step both modes hold the same state up to the forces' summation order (the
+    # second step can differ more: pairs at r ~ r_c may fall on either side after such changes)
+    a, b = union([o[0] for o in res[0]]), union([o[0] for o in res[1]])
+    for key in ("x", "y", "z"):
         assert np.allclose(a[key], b[key], rtol=0, atol=1e-6)
