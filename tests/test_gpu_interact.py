@@ -445,3 +445,25 @@ def test_out_of_box_flag():
         ctx.bin(*to_dev(c2))
         with pytest.raises(PiError, match="0x1"):
             ctx.stats()
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("algo", ["global", "fullload", "xpreg", "half"])
+def test_strategy_fuzz(algo, seed):
+    """Random grid shapes, densities, X sub-cells, kernels and (full load) sub-box shapes and
+    capacities for the other strategies, against the oracle."""
+    rng = np.random.default_rng(2000 + seed + 31 * ALGOS.index(algo))
+    dims = tuple(int(v) for v in rng.integers(3, 13, size=3))
+    ppc = float(rng.choice([1, 3, 8, 20]))
+    c = synth.scaled_uniform(ppc, dims, seed=300 + seed)
+    kernel = ["gaussian", "indicator", "candidate", "lj", "lowflop"][seed % 5]
+    xs = int(rng.choice([1, 2, 4]))
+    tune = {}
+    if algo == "fullload":
+        tune = dict(fullload_box=tuple(int(v) for v in rng.integers(1, 6, size=3)),
+                    fullload_cap=int(rng.choice([0, 64, 400])))
+    want = oracle_interact(c, kernel)
+    ctx = ctx_for(c, kernel, x_subcells=xs)
+    got, ctx = gpu_interact(c, algo, kernel, tuning=tune, ctx=ctx)
+    assert_parity(got, want, label=f"{algo} fuzz {seed} dims {dims} ppc {ppc} sx {xs} {kernel} {tune}")
+    assert ctx.stats()["candidates"] == int(want["C"].sum())
