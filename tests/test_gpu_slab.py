@@ -305,3 +305,57 @@ def test_slab_overlap_larger_sampled():
     a, b = union([o[0] for o in res[0]]), union([o[0] for o in res[1]])
     for key in ("x", "y", "z"):
         assert np.allclose(a[key], b[key], rtol=0, atol=1e-6)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_slab_fuzz(seed):
+    """Random X-slab runs: grid, density, P (dividing dims[0]), strategy, overlapped or serial and
+    two-phase or fixed-capacity exchange, two steps with migration; the union of the ranks' owned
+    particles is checked against the whole-cloud oracle after every step."""
+    rng = np.random.default_rng(4000 + seed)
+    nx = int(rng.choice([8, 12, 16]))
+    P = int(rng.choice([d for d in (2, 3, 4) if nx % d == 0]))
+    dims = (nx, int(rng.integers(3, 9)), int(rng.integers(3, 9)))
+    ppc = float(rng.choice([2, 6, 12]))
+    c = synth.scaled_uniform(ppc, dims, seed=500 + seed)
+    g = c.grid
+    algo = ["xpencil", "global", "half"][seed % 3]
+    tune = dict(exchange_overlap=int(rng.integers(0, 2)), exchange_full=int(rng.integers(0, 2)))
+    F = celllist.interact(c.x, c.y, c.z, c.q, g)["out"][:, 1:]
+    dt = float(np.float32(0.7 * g.w / np.abs(F).max()))
+    ctxs = _contexts(g, P, capacity=c.n)
+    parts = [_partition(c, k) for k in ctxs]
+
+    def run(r, k):
+        k.set_tuning(**tune)
+        idx = parts[r]
+        states = []
+        with torch.cuda.stream(k.stream):
+            k.bin(*(_dev(a[idx]) for a in (c.x, c.y, c.z, c.q)), id=_dev(idx.astype(np.int32)))
+            for _ in range(2):
+                k.step(algo, dt)
+                states.append({key: v.cpu().numpy() for key, v in k.get_particles().items()})
+        k.stream.synchronize()
+        return states, k.stats()
+
+    with cf.ThreadPoolExecutor(P) as pool:
+        res = _all(pool, run, ctxs)
+    for k in ctxs:
+        k.close()
+
+    def union(states):
+        d = {key: np.concatenate([s[key] for s in states]) for key in states[0]}
+        order = np.argsort(d["id"])
+        return {key: v[order] for key, v in d.items()}
+
+    prev = {"x": c.x, "y": c.y, "z": c.z, "q": c.q}
+    for it in range(2):
+        s1 = union([st[it] for st, _ in res])
+        assert np.array_equal(s1["id"], np.arange(c.n)), "a particle lost or duplicated"
+        want = celllist.interact(prev["x"], prev["y"], prev["z"], prev["q"], g)
+        got = np.stack([s1[k] for k in ("phi", "fx", "fy", "fz")], 1).astype(np.float64)
+        assert_parity(got, want, label=f"slab fuzz {seed} P={P} dims={dims} {algo} {tune} step {it}")
+        prev = s1
+    for _, st in res:
+        ovl = algo == "xpencil" and tune["exchange_overlap"] == 0 and nx // P >= 4
+        assert st["overlapped_steps"] == (2 if ovl else 0)
