@@ -359,3 +359,32 @@ def test_slab_fuzz(seed):
     for _, st in res:
         ovl = algo == "xpencil" and tune["exchange_overlap"] == 0 and nx // P >= 4
         assert st["overlapped_steps"] == (2 if ovl else 0)
+
+
+def test_slab_run_host():
+    """pi_run_host with X-slabs (the e2e path of bench.py at N > 1): each rank passes its slab's
+    particles in pinned host memory and gets its outputs back in caller order."""
+    c = synth.make_config("c0", n=4 * 4096)
+    g = c.grid
+    P = 2
+    ctxs = _contexts(g, P, capacity=c.n)
+    parts = [_partition(c, k) for k in ctxs]
+
+    def run(r, k):
+        idx = parts[r]
+        h = [torch.from_numpy(np.ascontiguousarray(a[idx])).pin_memory() for a in (c.x, c.y, c.z, c.q)]
+        o = [torch.empty(len(idx), dtype=torch.float32).pin_memory() for _ in range(4)]
+        with torch.cuda.stream(k.stream):
+            k.run_host("xpencil", *h, *o)
+            k.run_host("xpencil", *h, *o)  # twice: the second reuses the context's state
+        k.stream.synchronize()
+        return torch.stack(o, 1).numpy().astype(np.float64)
+
+    with cf.ThreadPoolExecutor(P) as pool:
+        res = _all(pool, run, ctxs)
+    for k in ctxs:
+        k.close()
+    got = np.zeros((c.n, 4))
+    for r in range(P):
+        got[parts[r]] = res[r]
+    assert_parity(got, celllist.interact(c.x, c.y, c.z, c.q, g), label="slab run_host")
